@@ -1,0 +1,244 @@
+"""Thin ctypes binding over libnbody.so (include/nbody.h).
+
+Argument marshalling only: every step of the hot path runs in the library's
+CUDA kernels.  Tensors may be torch tensors (CUDA or CPU) or numpy arrays;
+they are passed to the C-ABI as raw pointers.  There is no fallback: if the
+library or a CUDA device is missing, construction raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+from . import _build
+
+NBODY_OK, NBODY_EINVAL, NBODY_ENONFINITE, NBODY_ECUDA, NBODY_ENCCL, NBODY_ENOMEM, NBODY_ESTATE = range(7)
+NBODY_HERMITE4, NBODY_LEAPFROG_KDK = 0, 1
+
+EXPORTS = (
+    "nbody_plan", "nbody_nccl_unique_id", "nbody_init", "nbody_local_range",
+    "nbody_compute_forces", "nbody_step", "nbody_energy", "nbody_get_state",
+    "nbody_set_state", "nbody_sync", "nbody_prof_enable", "nbody_prof_read",
+    "nbody_last_error", "nbody_destroy",
+)
+
+
+class NBodyError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"[nbody status {code}] {msg}")
+        self.code = code
+
+
+class Config(ctypes.Structure):
+    _fields_ = [
+        ("n", ctypes.c_int64),
+        ("G", ctypes.c_double),
+        ("eps", ctypes.c_double),
+        ("dt", ctypes.c_double),
+        ("integrator", ctypes.c_int32),
+        ("device", ctypes.c_int32),
+        ("rank", ctypes.c_int32),
+        ("world", ctypes.c_int32),
+        ("loopback", ctypes.c_int32),
+        ("jchunks", ctypes.c_int32),
+        ("nccl_id", ctypes.c_void_p),
+        ("stream", ctypes.c_void_p),
+    ]
+
+
+_lib = None
+
+
+def _set_nccl_path():
+    if os.environ.get("NBODY_NCCL_LIB"):
+        return
+    try:
+        import nvidia.nccl
+        p = os.path.join(list(nvidia.nccl.__path__)[0], "lib", "libnccl.so.2")
+        if os.path.exists(p):
+            os.environ["NBODY_NCCL_LIB"] = p   # the NCCL torch itself loads
+    except Exception:
+        pass
+
+
+def lib():
+    """Load (building first if missing or stale) libnbody.so."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    path = _build.build() if _build.stale() else _build.LIB
+    _set_nccl_path()
+    L = ctypes.CDLL(path)
+    i32, i64, p, d = ctypes.c_int32, ctypes.c_int64, ctypes.c_void_p, ctypes.c_double
+    P64 = ctypes.POINTER(i64)
+    Pd = ctypes.POINTER(d)
+    sig = {
+        "nbody_plan": ([i64, i32, i32, i32, P64, P64, P64, P64, P64], ctypes.c_int),
+        "nbody_nccl_unique_id": ([p], ctypes.c_int),
+        "nbody_init": ([ctypes.POINTER(Config), p, p, p, ctypes.POINTER(p)], ctypes.c_int),
+        "nbody_local_range": ([p, P64, P64], ctypes.c_int),
+        "nbody_compute_forces": ([p, p, p], ctypes.c_int),
+        "nbody_step": ([p, i32], ctypes.c_int),
+        "nbody_energy": ([p, Pd, Pd], ctypes.c_int),
+        "nbody_get_state": ([p, p, p], ctypes.c_int),
+        "nbody_set_state": ([p, p, p, i32], ctypes.c_int),
+        "nbody_sync": ([p], ctypes.c_int),
+        "nbody_prof_enable": ([p, i32], ctypes.c_int),
+        "nbody_prof_read": ([p, Pd, P64, P64, i32], ctypes.c_int),
+        "nbody_last_error": ([p], ctypes.c_char_p),
+        "nbody_destroy": ([p], None),
+    }
+    for name, (args, res) in sig.items():
+        f = getattr(L, name)
+        f.argtypes = args
+        f.restype = res
+    _lib = L
+    return L
+
+
+def _check(rc, ctx=None):
+    if rc != NBODY_OK:
+        msg = lib().nbody_last_error(ctx).decode()
+        raise NBodyError(rc, msg)
+
+
+def plan(n, world=1, rank=0, jchunks=0):
+    """Partition / reduction plan (host-only): dict(i0, i1, slot, chunk, n_chunks)."""
+    out = [ctypes.c_int64() for _ in range(5)]
+    _check(lib().nbody_plan(n, world, rank, jchunks, *[ctypes.byref(o) for o in out]))
+    return dict(zip(("i0", "i1", "slot", "chunk", "n_chunks"), (o.value for o in out)))
+
+
+def nccl_unique_id() -> bytes:
+    buf = (ctypes.c_uint8 * 128)()
+    _check(lib().nbody_nccl_unique_id(buf))
+    return bytes(buf)
+
+
+def _ptr(a):
+    """Raw data pointer of a contiguous float64 torch tensor / numpy array."""
+    if a is None:
+        return None
+    if isinstance(a, np.ndarray):
+        if a.dtype != np.float64 or not a.flags.c_contiguous:
+            raise ValueError("numpy arrays must be C-contiguous float64")
+        return a.ctypes.data
+    import torch
+    if isinstance(a, torch.Tensor):
+        if a.dtype != torch.float64 or not a.is_contiguous():
+            raise ValueError("tensors must be contiguous float64")
+        return a.data_ptr()
+    raise TypeError(f"unsupported array type {type(a)}")
+
+
+class NBody:
+    """One rank's (or, with loopback=True, all ranks') view of an N-body system.
+
+    m: (n,), x, v: (3, n) float64 of the FULL system (torch CUDA/CPU tensors or
+    numpy).  Work is ordered on ``stream`` (a torch.cuda.Stream, a raw
+    cudaStream_t int, or None for torch's current stream).
+    """
+
+    def __init__(self, m, x, v, eps, dt, G=1.0, integrator="hermite", rank=0, world=1,
+                 loopback=False, nccl_id=None, device=None, stream=None, jchunks=0):
+        import torch
+        if not torch.cuda.is_available():
+            raise NBodyError(NBODY_ECUDA, "no CUDA device: libnbody has no CPU path")
+        if device is None:
+            device = torch.cuda.current_device()
+        if stream is None:
+            stream = torch.cuda.current_stream(device)
+        self.stream = stream
+        raw_stream = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+        self._keep = []
+        m, x, v = (self._prep(a) for a in (m, x, v))
+        n = int(m.shape[0])
+        cfg = Config(n=n, G=float(G), eps=float(eps), dt=float(dt),
+                     integrator={"hermite": NBODY_HERMITE4, "leapfrog": NBODY_LEAPFROG_KDK}[integrator],
+                     device=int(device), rank=int(rank), world=int(world),
+                     loopback=1 if loopback else 0, jchunks=int(jchunks),
+                     nccl_id=None, stream=raw_stream)
+        if nccl_id is not None:
+            idbuf = (ctypes.c_uint8 * 128).from_buffer_copy(nccl_id)
+            self._keep.append(idbuf)
+            cfg.nccl_id = ctypes.addressof(idbuf)
+        self.cfg = cfg
+        self.n = n
+        self.device = torch.device("cuda", int(device))
+        ctx = ctypes.c_void_p()
+        _check(lib().nbody_init(ctypes.byref(cfg), _ptr(m), _ptr(x), _ptr(v), ctypes.byref(ctx)))
+        self._ctx = ctx
+        i0, i1 = ctypes.c_int64(), ctypes.c_int64()
+        _check(lib().nbody_local_range(ctx, ctypes.byref(i0), ctypes.byref(i1)), ctx)
+        self.i0, self.i1 = i0.value, i1.value
+        self.n_loc = self.i1 - self.i0
+
+    @staticmethod
+    def _prep(a):
+        if isinstance(a, np.ndarray):
+            return np.ascontiguousarray(a, dtype=np.float64)
+        return a.contiguous().to(dtype=__import__("torch").float64)
+
+    def _c(self, rc):
+        _check(rc, self._ctx)
+
+    def forces(self, acc=None, jerk=None):
+        """(acc, jerk) of the local particles, (3, n_loc) float64 CUDA tensors."""
+        import torch
+        if acc is None:
+            acc = torch.empty((3, self.n_loc), dtype=torch.float64, device=self.device)
+        if jerk is None:
+            jerk = torch.empty((3, self.n_loc), dtype=torch.float64, device=self.device)
+        self._c(lib().nbody_compute_forces(self._ctx, _ptr(acc), _ptr(jerk)))
+        return acc, jerk
+
+    def step(self, nsteps=1):
+        self._c(lib().nbody_step(self._ctx, int(nsteps)))
+
+    def energy(self):
+        ke, pe = ctypes.c_double(), ctypes.c_double()
+        self._c(lib().nbody_energy(self._ctx, ctypes.byref(ke), ctypes.byref(pe)))
+        return ke.value, pe.value
+
+    def state(self, x=None, v=None):
+        import torch
+        if x is None:
+            x = torch.empty((3, self.n_loc), dtype=torch.float64, device=self.device)
+        if v is None:
+            v = torch.empty((3, self.n_loc), dtype=torch.float64, device=self.device)
+        self._c(lib().nbody_get_state(self._ctx, _ptr(x), _ptr(v)))
+        return x, v
+
+    def set_state(self, x, v, keep_forces=False):
+        self._c(lib().nbody_set_state(self._ctx, _ptr(x), _ptr(v), 1 if keep_forces else 0))
+
+    def sync(self):
+        self._c(lib().nbody_sync(self._ctx))
+
+    def prof_enable(self, on=True):
+        self._c(lib().nbody_prof_enable(self._ctx, 1 if on else 0))
+
+    def prof_read(self, reset=True):
+        ms, nf, nk = ctypes.c_double(), ctypes.c_int64(), ctypes.c_int64()
+        self._c(lib().nbody_prof_read(self._ctx, ctypes.byref(ms), ctypes.byref(nf),
+                                      ctypes.byref(nk), 1 if reset else 0))
+        return ms.value, nf.value, nk.value
+
+    def close(self):
+        if getattr(self, "_ctx", None):
+            lib().nbody_destroy(self._ctx)
+            self._ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()

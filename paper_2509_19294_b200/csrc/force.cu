@@ -1,0 +1,268 @@
+// force.cu -- the hot loop: softened acceleration + jerk, all i x all j,
+// FP32 pair arithmetic on sm_100a packed FP32x2 (FFMA2/FADD2/FMUL2) plus
+// MUFU.RSQ, j-tiles staged in shared memory by bulk TMA (cp.async.bulk)
+// into an mbarrier ring.
+//
+// What it computes (P:134-138 [Sec. 3, force equation]; softening R#1; jerk
+// R#2): for every local i and every j of the chunk
+//     d = x_j - x_i, w = v_j - v_i, s = |d|^2 + eps^2
+//     a_i += G m_j d / s^{3/2}
+//     j_i += G m_j (w - 3 (d.w) d / s) / s^{3/2}
+// in FP32 ("acceleration, jerk, and other intermediate values ... in
+// single precision"), summed sequentially over the 256 j of a tile, the
+// tile sums added in fp64 in ascending tile order; the fp64 chunk sum is
+// written to partial[chunk][6][i].  Chunks are folded in ascending order by
+// the fp64 particle-update kernels (hermite.cu), so the grouping of every
+// floating-point operation is fixed by (n, chunk) alone (R#10).
+//
+// Mapping (B200 redesign of the paper's core/tile mapping):
+//   CTA  = (i-block of kI = 2 * kPairs * kThreads particles, j-chunk)
+//   thread = kPairs packed i-pairs in registers (x_i, v_i negated so every
+//            difference is one FADD2 with the broadcast j operand)
+//   j      = broadcast from shared memory (LDS.128 x 2 per j per thread)
+//   producer = thread 0 issues cp.async.bulk of 8 KiB tiles (the paper's
+//            `read` kernel + circular buffers, as TMA + mbarriers)
+#include "internal.h"
+
+namespace nb {
+
+namespace {
+
+constexpr int kThreads = 128;
+constexpr int kPairs = 2;                 // i-pairs per thread (4 i)
+constexpr int kStages = 2;                // smem ring depth (tiles)
+constexpr int kIPerBlock = 2 * kPairs * kThreads;
+constexpr int kTileBytes = kTile * (int)sizeof(JPkt);
+constexpr int kSmemBytes = kStages * kTileBytes + 64;
+
+typedef unsigned long long f2;  // packed {lo, hi} fp32 pair in one 64-bit register
+
+__device__ __forceinline__ f2 f2make(float lo, float hi) {
+    f2 r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+    return r;
+}
+__device__ __forceinline__ f2 f2bc(float a) { return f2make(a, a); }
+__device__ __forceinline__ void f2split(f2 a, float& lo, float& hi) {
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(a));
+}
+__device__ __forceinline__ f2 fadd2(f2 a, f2 b) {
+    f2 d;
+    asm("add.rn.ftz.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ f2 fmul2(f2 a, f2 b) {
+    f2 d;
+    asm("mul.rn.ftz.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ f2 ffma2(f2 a, f2 b, f2 c) {
+    f2 d;
+    asm("fma.rn.ftz.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
+}
+__device__ __forceinline__ float rsqrt_ftz(float s) {
+    float r;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(s));
+    return r;
+}
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(smem_addr(bar)), "r"(parity)
+            : "memory");
+    }
+}
+// 1-D bulk TMA global -> shared, completion counted on `bar` (UBLKCP in SASS)
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes,
+                                            uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_addr(dst)),
+        "l"(src), "r"(bytes), "r"(smem_addr(bar))
+        : "memory");
+}
+
+template <bool kGuard>
+__global__ void __launch_bounds__(kThreads, 3) force_kernel(ForceArgs a) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    JPkt* ring = reinterpret_cast<JPkt*>(smem);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kTileBytes);
+
+    const int tid = threadIdx.x;
+    const int c = (a.c_first + (int)blockIdx.y) % a.n_chunks;
+    const int64_t jc0 = (int64_t)c * a.chunk;
+    const int ntile = a.chunk / kTile;
+    const int ib = (int)blockIdx.x * kIPerBlock;
+
+    // ---- i-particles: kPairs packed pairs, stored negated (d = x_j + (-x_i))
+    f2 nx[kPairs], ny[kPairs], nz[kPairs], nvx[kPairs], nvy[kPairs], nvz[kPairs];
+#pragma unroll
+    for (int p = 0; p < kPairs; ++p) {
+        float q[2][6];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int il = ib + (2 * p + h) * kThreads + tid;
+            if (il < a.n_loc) {
+                const JPkt pk = a.pkt[a.i_base + il];
+                q[h][0] = -pk.p.x; q[h][1] = -pk.p.y; q[h][2] = -pk.p.z;
+                q[h][3] = -pk.v.x; q[h][4] = -pk.v.y; q[h][5] = -pk.v.z;
+            } else {  // padding i: computed, never stored
+                q[h][0] = q[h][1] = q[h][2] = 0.f;
+                q[h][3] = q[h][4] = q[h][5] = 0.f;
+            }
+        }
+        nx[p] = f2make(q[0][0], q[1][0]);
+        ny[p] = f2make(q[0][1], q[1][1]);
+        nz[p] = f2make(q[0][2], q[1][2]);
+        nvx[p] = f2make(q[0][3], q[1][3]);
+        nvy[p] = f2make(q[0][4], q[1][4]);
+        nvz[p] = f2make(q[0][5], q[1][5]);
+    }
+
+    double acc64[6][2 * kPairs];
+#pragma unroll
+    for (int k = 0; k < 6; ++k)
+#pragma unroll
+        for (int l = 0; l < 2 * kPairs; ++l) acc64[k][l] = 0.0;
+
+    if (tid == 0) {
+#pragma unroll
+        for (int s = 0; s < kStages; ++s) mbar_init(&full[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (tid == 0) {
+        for (int s = 0; s < kStages && s < ntile; ++s) {
+            mbar_expect_tx(&full[s], kTileBytes);
+            tma_load_1d(ring + s * kTile, a.pkt + jc0 + (int64_t)s * kTile, kTileBytes, &full[s]);
+        }
+    }
+
+    const f2 eps2 = f2bc(a.eps2);
+    const f2 m3 = f2bc(-3.0f);
+
+    for (int t = 0; t < ntile; ++t) {
+        const int s = t % kStages;
+        mbar_wait(&full[s], (uint32_t)((t / kStages) & 1));
+        const JPkt* tile = ring + s * kTile;
+
+        f2 ax[kPairs], ay[kPairs], az[kPairs], jx[kPairs], jy[kPairs], jz[kPairs];
+#pragma unroll
+        for (int p = 0; p < kPairs; ++p) ax[p] = ay[p] = az[p] = jx[p] = jy[p] = jz[p] = 0ull;
+
+#pragma unroll 4
+        for (int jj = 0; jj < kTile; ++jj) {
+            const float4 P = tile[jj].p;
+            const float4 V = tile[jj].v;
+            const f2 xj = f2bc(P.x), yj = f2bc(P.y), zj = f2bc(P.z), mj = f2bc(P.w);
+            const f2 vxj = f2bc(V.x), vyj = f2bc(V.y), vzj = f2bc(V.z);
+#pragma unroll
+            for (int p = 0; p < kPairs; ++p) {
+                const f2 dx = fadd2(xj, nx[p]);
+                const f2 dy = fadd2(yj, ny[p]);
+                const f2 dz = fadd2(zj, nz[p]);
+                const f2 wx = fadd2(vxj, nvx[p]);
+                const f2 wy = fadd2(vyj, nvy[p]);
+                const f2 wz = fadd2(vzj, nvz[p]);
+                f2 s2 = ffma2(dx, dx, eps2);
+                s2 = ffma2(dy, dy, s2);
+                s2 = ffma2(dz, dz, s2);
+                float s_lo, s_hi;
+                f2split(s2, s_lo, s_hi);
+                float r_lo = rsqrt_ftz(s_lo), r_hi = rsqrt_ftz(s_hi);
+                if (kGuard) {  // eps == 0: exclude j == i (s == 0), R#17
+                    if (s_lo == 0.f) {
+                        r_lo = 0.f;
+                        const int64_t ig = a.i_base + ib + (2 * p) * kThreads + tid;
+                        const int64_t jg = jc0 + (int64_t)t * kTile + jj;
+                        if (ig != jg && ig < a.i_base + a.n_loc && P.w != 0.f)
+                            atomicMin(a.coincident, (unsigned long long)ig);
+                    }
+                    if (s_hi == 0.f) {
+                        r_hi = 0.f;
+                        const int64_t ig = a.i_base + ib + (2 * p + 1) * kThreads + tid;
+                        const int64_t jg = jc0 + (int64_t)t * kTile + jj;
+                        if (ig != jg && ig < a.i_base + a.n_loc && P.w != 0.f)
+                            atomicMin(a.coincident, (unsigned long long)ig);
+                    }
+                }
+                const f2 ri = f2make(r_lo, r_hi);
+                const f2 ri2 = fmul2(ri, ri);
+                const f2 mr3 = fmul2(fmul2(mj, ri), ri2);      // G m_j / s^{3/2}
+                f2 rv = fmul2(dx, wx);
+                rv = ffma2(dy, wy, rv);
+                rv = ffma2(dz, wz, rv);                         // d . w
+                const f2 q3 = fmul2(fmul2(rv, ri2), m3);        // -3 (d.w) / s
+                ax[p] = ffma2(mr3, dx, ax[p]);
+                ay[p] = ffma2(mr3, dy, ay[p]);
+                az[p] = ffma2(mr3, dz, az[p]);
+                jx[p] = ffma2(mr3, ffma2(q3, dx, wx), jx[p]);
+                jy[p] = ffma2(mr3, ffma2(q3, dy, wy), jy[p]);
+                jz[p] = ffma2(mr3, ffma2(q3, dz, wz), jz[p]);
+            }
+        }
+        // tile sum -> fp64, ascending tile order
+#pragma unroll
+        for (int p = 0; p < kPairs; ++p) {
+            float lo, hi;
+            f2split(ax[p], lo, hi); acc64[0][2 * p] += (double)lo; acc64[0][2 * p + 1] += (double)hi;
+            f2split(ay[p], lo, hi); acc64[1][2 * p] += (double)lo; acc64[1][2 * p + 1] += (double)hi;
+            f2split(az[p], lo, hi); acc64[2][2 * p] += (double)lo; acc64[2][2 * p + 1] += (double)hi;
+            f2split(jx[p], lo, hi); acc64[3][2 * p] += (double)lo; acc64[3][2 * p + 1] += (double)hi;
+            f2split(jy[p], lo, hi); acc64[4][2 * p] += (double)lo; acc64[4][2 * p + 1] += (double)hi;
+            f2split(jz[p], lo, hi); acc64[5][2 * p] += (double)lo; acc64[5][2 * p + 1] += (double)hi;
+        }
+        __syncthreads();  // every warp is done reading stage s
+        if (tid == 0 && t + kStages < ntile) {
+            mbar_expect_tx(&full[s], kTileBytes);
+            tma_load_1d(ring + s * kTile, a.pkt + jc0 + (int64_t)(t + kStages) * kTile, kTileBytes,
+                        &full[s]);
+        }
+    }
+
+    // chunk partial, coalesced fp64 stores
+    double* out = a.partial + (int64_t)c * 6 * a.n_loc_pad;
+#pragma unroll
+    for (int l = 0; l < 2 * kPairs; ++l) {
+        const int il = ib + l * kThreads + tid;
+        if (il < a.n_loc) {
+#pragma unroll
+            for (int k = 0; k < 6; ++k) out[(int64_t)k * a.n_loc_pad + il] = acc64[k][l];
+        }
+    }
+}
+
+}  // namespace
+
+int force_i_per_block() { return kIPerBlock; }
+
+cudaError_t launch_force(const ForceArgs& a, bool guard_self, cudaStream_t s) {
+    if (a.c_count <= 0 || a.n_loc <= 0) return cudaSuccess;
+    dim3 grid((unsigned)((a.n_loc + kIPerBlock - 1) / kIPerBlock), (unsigned)a.c_count);
+    if (guard_self)
+        force_kernel<true><<<grid, kThreads, kSmemBytes, s>>>(a);
+    else
+        force_kernel<false><<<grid, kThreads, kSmemBytes, s>>>(a);
+    return cudaGetLastError();
+}
+
+}  // namespace nb

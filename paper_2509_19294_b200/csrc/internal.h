@@ -1,0 +1,67 @@
+// internal.h -- shared declarations of the libnbody kernels and runtime.
+// Product code only; nothing here is shared with oracle/.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace nb {
+
+// j-particle packet, 32 B, the B200 replacement of the paper's replicated
+// 32x32 tiles: one float4 position + G*m, one float4 velocity.
+struct __align__(16) JPkt {
+    float4 p;  // x, y, z, G*m      (fp32, RNE from fp64 state)
+    float4 v;  // vx, vy, vz, 0
+};
+
+constexpr int kTile = 256;  // j per fp32 partial-sum tile (R#10)
+
+// Force pass arguments.  One CTA = (i-block, chunk); see force.cu.
+struct ForceArgs {
+    const JPkt* pkt;     // all-gathered j packets [L]
+    int64_t i_base;      // global index of local particle 0
+    int32_t n_loc;       // local particles
+    int64_t n_loc_pad;   // row stride of `partial`
+    int32_t chunk;       // j per chunk (multiple of kTile)
+    int32_t n_chunks;    // chunks in the canonical order
+    int32_t c_first;     // first chunk of this launch
+    int32_t c_count;     // chunks in this launch (grid.y)
+    float eps2;          // fp32(eps^2)
+    double* partial;     // [n_chunks][6][n_loc_pad] (acc x,y,z, jerk x,y,z)
+    unsigned long long* coincident;  // eps == 0 only: min global i of a coincident pair
+};
+
+// Launches the force pass for chunks c_first .. c_first + c_count - 1 (mod
+// n_chunks) over all local i.  Returns the launch error.
+cudaError_t launch_force(const ForceArgs& a, bool guard_self, cudaStream_t s);
+int force_i_per_block();
+
+// fp64 particle-update kernels (hermite.cu).
+struct StateArgs {
+    int32_t n_loc;
+    int64_t n_loc_pad;   // row stride of x, v, a0, j0, xp, vp, partial
+    int64_t i_base;      // global index of local particle 0
+    double G, dt;
+    const double* m;     // [n_loc]
+    double *x, *v, *a0, *j0, *xp, *vp;  // [3][n_loc_pad]
+    const double* partial;  // [n_chunks][6][n_loc_pad]
+    int32_t n_chunks;
+    JPkt* pkt;           // all packets; local particle i goes to pkt[i_base + i]
+    unsigned long long* bad;  // min global index of a non-finite particle
+};
+cudaError_t launch_pack_state(const StateArgs& a, cudaStream_t s);     // x, v -> pkt
+cudaError_t launch_predict_pack(const StateArgs& a, cudaStream_t s);   // x,v,a0,j0 -> xp,vp,pkt
+cudaError_t launch_fold_forces(const StateArgs& a, cudaStream_t s);    // partial -> a0, j0
+cudaError_t launch_correct_predict_pack(const StateArgs& a, cudaStream_t s);
+cudaError_t launch_fill_padding(JPkt* pkt, int64_t from, int64_t to, cudaStream_t s);
+// bad2[0]: min global index with m not finite or <= 0; bad2[1]: x or v not finite
+cudaError_t launch_validate(const StateArgs& a, unsigned long long* bad2, cudaStream_t s);
+
+// fp64 energy (energy.cu).  eall: [L] (x, y, z, m) of every particle.
+cudaError_t launch_energy_pack(const StateArgs& a, double4* eall, cudaStream_t s);
+cudaError_t launch_energy(const double4* eall, int64_t n, int64_t i_base,
+                          int32_t n_loc, const double* v, int64_t n_loc_pad,
+                          const double* m, double eps2, double* block_sums,
+                          int nblocks_max, double* out2, cudaStream_t s);
+int energy_blocks(int32_t n_loc);
+
+}  // namespace nb

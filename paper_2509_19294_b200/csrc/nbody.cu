@@ -1,0 +1,661 @@
+// nbody.cu -- the C-ABI runtime of libnbody.so (declared in include/nbody.h).
+//
+// Owns the device state of one rank (or of all ranks in loopback mode),
+// the exchange buffer, the CUDA events/streams and the NCCL communicator,
+// and sequences the per-step kernels:
+//
+//   predict+pack (fp64 -> fp32 packets)            hermite.cu
+//   exchange: ncclAllGather of 32-B packets         (P > 1; comm stream)
+//   force pass over the local j-chunks              force.cu   -- overlaps the
+//   force pass over the remote j-chunks             force.cu      all-gather
+//   fold chunks + correct + predict + pack (fp64)   hermite.cu
+//
+// NCCL is resolved with dlopen at first use (the libnccl.so.2 the process
+// already loaded, i.e. torch's, unless NBODY_NCCL_LIB names another), so the
+// library never links a second NCCL and never needs one for world == 1.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <climits>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "internal.h"
+#include "nbody.h"
+
+using nb::JPkt;
+
+namespace {
+
+thread_local std::string g_last_error = "";
+
+// ------------------------------------------------------------------ NCCL
+
+struct NcclApi {
+    bool tried = false, ok = false;
+    std::string why;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;
+    ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
+                              cudaStream_t) = nullptr;
+    const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+NcclApi& nccl() {
+    static NcclApi api;
+    if (api.tried) return api;
+    api.tried = true;
+    const char* path = getenv("NBODY_NCCL_LIB");
+    void* h = dlopen(path && *path ? path : "libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+        api.why = std::string("cannot load NCCL: ") + dlerror();
+        return api;
+    }
+#define NB_SYM(field, name)                                         \
+    api.field = reinterpret_cast<decltype(api.field)>(dlsym(h, name)); \
+    if (!api.field) {                                                \
+        api.why = std::string("NCCL symbol missing: ") + name;       \
+        return api;                                                  \
+    }
+    NB_SYM(GetUniqueId, "ncclGetUniqueId");
+    NB_SYM(CommInitRank, "ncclCommInitRank");
+    NB_SYM(CommDestroy, "ncclCommDestroy");
+    NB_SYM(CommGetAsyncError, "ncclCommGetAsyncError");
+    NB_SYM(AllGather, "ncclAllGather");
+    NB_SYM(GetErrorString, "ncclGetErrorString");
+#undef NB_SYM
+    api.ok = true;
+    return api;
+}
+
+// ------------------------------------------------------------------ plan
+
+struct Plan {
+    int64_t i0, i1, slot, chunk, n_chunks;
+};
+
+int make_plan(int64_t n, int32_t world, int32_t rank, int32_t jchunks, Plan* p, std::string* why) {
+    if (n < 2) { *why = "n must be >= 2"; return NBODY_EINVAL; }
+    if (world < 1 || world > n) { *why = "world must satisfy 1 <= world <= n"; return NBODY_EINVAL; }
+    if (rank < 0 || rank >= world) { *why = "rank must satisfy 0 <= rank < world"; return NBODY_EINVAL; }
+    if (jchunks < 0) { *why = "jchunks must be >= 0"; return NBODY_EINVAL; }
+    const int64_t jc = jchunks == 0 ? 128 : jchunks;
+    const int64_t T = nb::kTile;
+    p->slot = T * ((n + T * world - 1) / (T * world));
+    p->i0 = std::min<int64_t>(n, rank * p->slot);
+    p->i1 = std::min<int64_t>(n, (int64_t)(rank + 1) * p->slot);
+    p->chunk = T * ((n + T * jc - 1) / (T * jc));
+    p->n_chunks = (n + p->chunk - 1) / p->chunk;
+    return NBODY_OK;
+}
+
+// ------------------------------------------------------------------ context
+
+struct Shard {
+    Plan plan;
+    int32_t n_loc = 0;
+    int64_t n_loc_pad = 0;
+    double *m = nullptr, *x = nullptr, *v = nullptr, *a0 = nullptr, *j0 = nullptr;
+    double *xp = nullptr, *vp = nullptr, *partial = nullptr;
+    int32_t c_lo = 0, c_hi = 0;  // local chunks [c_lo, c_hi)
+};
+
+bool is_device_ptr(const void* p) {
+    if (!p) return false;
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+}  // namespace
+
+struct nbody_ctx {
+    nbody_config cfg{};
+    int64_t n = 0, L = 0;
+    float eps2f = 0.f;
+    int nshards = 1;
+    std::vector<Shard> sh;
+    JPkt* pkt = nullptr;
+    double4* eall = nullptr;
+    double* eblk = nullptr;
+    int eblk_cap = 0;
+    double* eout = nullptr;  // [nshards][2]
+    unsigned long long* flags = nullptr;  // [0] non-finite, [1] coincident, [2..3] validate
+    cudaStream_t stream = nullptr, comm_stream = nullptr;
+    bool own_stream = false;
+    cudaEvent_t ev_packed = nullptr, ev_gathered = nullptr;
+    ncclComm_t comm = nullptr;
+    bool have_a0 = false, predicted = false;
+    bool prof = false;
+    std::vector<cudaEvent_t> prof_ev;  // pairs
+    size_t prof_used = 0;
+    int64_t n_force = 0, n_kernels = 0;
+    std::string err;
+    int sticky = 0;
+};
+
+namespace {
+
+int fail(nbody_ctx* c, int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    if (c) {
+        c->err = buf;
+        if (code == NBODY_ECUDA || code == NBODY_ENCCL || code == NBODY_ENONFINITE) c->sticky = code;
+    }
+    g_last_error = buf;
+    return code;
+}
+
+#define CK(ctx, call)                                                                      \
+    do {                                                                                   \
+        cudaError_t e_ = (call);                                                           \
+        if (e_ != cudaSuccess)                                                             \
+            return fail(ctx, NBODY_ECUDA, "%s failed: %s (%s:%d)", #call,                  \
+                        cudaGetErrorString(e_), __FILE__, __LINE__);                       \
+    } while (0)
+
+#define CKNCCL(ctx, call)                                                                  \
+    do {                                                                                   \
+        ncclResult_t r_ = (call);                                                          \
+        if (r_ != ncclSuccess)                                                             \
+            return fail(ctx, NBODY_ENCCL, "%s failed: %s", #call, nccl().GetErrorString(r_)); \
+    } while (0)
+
+#define GUARD(ctx)                                                                          \
+    do {                                                                                    \
+        if (!(ctx)) return fail(nullptr, NBODY_EINVAL, "null context");                     \
+        if ((ctx)->sticky)                                                                  \
+            return fail(ctx, NBODY_ESTATE, "context failed earlier: %s", (ctx)->err.c_str()); \
+        CK(ctx, cudaSetDevice((ctx)->cfg.device));                                          \
+    } while (0)
+
+nb::StateArgs state_args(nbody_ctx* c, Shard& s) {
+    nb::StateArgs a;
+    a.n_loc = s.n_loc;
+    a.n_loc_pad = s.n_loc_pad;
+    a.i_base = s.plan.i0;
+    a.G = c->cfg.G;
+    a.dt = c->cfg.dt;
+    a.m = s.m;
+    a.x = s.x; a.v = s.v; a.a0 = s.a0; a.j0 = s.j0; a.xp = s.xp; a.vp = s.vp;
+    a.partial = s.partial;
+    a.n_chunks = (int32_t)s.plan.n_chunks;
+    a.pkt = c->pkt;
+    a.bad = c->flags;
+    return a;
+}
+
+bool use_nccl(const nbody_ctx* c) { return c->comm != nullptr; }
+
+int launch_force_range(nbody_ctx* c, Shard& s, int32_t c_first, int32_t c_count) {
+    if (c_count <= 0 || s.n_loc <= 0) return NBODY_OK;
+    nb::ForceArgs f;
+    f.pkt = c->pkt;
+    f.i_base = s.plan.i0;
+    f.n_loc = s.n_loc;
+    f.n_loc_pad = s.n_loc_pad;
+    f.chunk = (int32_t)s.plan.chunk;
+    f.n_chunks = (int32_t)s.plan.n_chunks;
+    f.c_first = c_first;
+    f.c_count = c_count;
+    f.eps2 = c->eps2f;
+    f.partial = s.partial;
+    f.coincident = c->flags + 1;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (c->prof) {
+        if (c->prof_used + 2 > c->prof_ev.size()) {
+            for (int k = 0; k < 2; ++k) {
+                cudaEvent_t e;
+                CK(c, cudaEventCreate(&e));
+                c->prof_ev.push_back(e);
+            }
+        }
+        e0 = c->prof_ev[c->prof_used];
+        e1 = c->prof_ev[c->prof_used + 1];
+        c->prof_used += 2;
+        CK(c, cudaEventRecord(e0, c->stream));
+    }
+    CK(c, nb::launch_force(f, c->eps2f == 0.f, c->stream));
+    if (e1) CK(c, cudaEventRecord(e1, c->stream));
+    c->n_force++;
+    c->n_kernels++;
+    return NBODY_OK;
+}
+
+// exchange the packets written by every shard's pack kernel, then run the
+// force pass of every shard: local chunks first (overlapping the
+// all-gather), remote chunks after it.
+int exchange_and_force(nbody_ctx* c) {
+    int rc;
+    if (use_nccl(c)) {
+        Shard& s = c->sh[0];
+        CK(c, cudaEventRecord(c->ev_packed, c->stream));
+        CK(c, cudaStreamWaitEvent(c->comm_stream, c->ev_packed, 0));
+        float* base = reinterpret_cast<float*>(c->pkt);
+        const size_t cnt = (size_t)s.plan.slot * 8;
+        CKNCCL(c, nccl().AllGather(base + (size_t)c->cfg.rank * cnt, base, cnt, ncclFloat32, c->comm,
+                                   c->comm_stream));
+        CK(c, cudaEventRecord(c->ev_gathered, c->comm_stream));
+        if ((rc = launch_force_range(c, s, s.c_lo, s.c_hi - s.c_lo))) return rc;
+        CK(c, cudaStreamWaitEvent(c->stream, c->ev_gathered, 0));
+        const int32_t nrem = (int32_t)s.plan.n_chunks - (s.c_hi - s.c_lo);
+        if ((rc = launch_force_range(c, s, s.c_hi % (int32_t)s.plan.n_chunks, nrem))) return rc;
+    } else {
+        // world == 1 or loopback: every packet already sits in c->pkt
+        for (auto& s : c->sh)
+            if ((rc = launch_force_range(c, s, 0, (int32_t)s.plan.n_chunks))) return rc;
+    }
+    return NBODY_OK;
+}
+
+int ensure_forces(nbody_ctx* c) {
+    if (c->have_a0) return NBODY_OK;
+    int rc;
+    for (auto& s : c->sh) {
+        CK(c, nb::launch_pack_state(state_args(c, s), c->stream));
+        c->n_kernels++;
+    }
+    if ((rc = exchange_and_force(c))) return rc;
+    for (auto& s : c->sh) {
+        CK(c, nb::launch_fold_forces(state_args(c, s), c->stream));
+        c->n_kernels++;
+    }
+    c->have_a0 = true;
+    c->predicted = false;
+    return NBODY_OK;
+}
+
+int check_flags(nbody_ctx* c) {
+    unsigned long long h[2];
+    CK(c, cudaMemcpyAsync(h, c->flags, sizeof h, cudaMemcpyDeviceToHost, c->stream));
+    CK(c, cudaStreamSynchronize(c->stream));
+    if (h[1] != ULLONG_MAX)
+        return fail(c, NBODY_ENONFINITE, "coincident pair involving particle %llu with eps = 0", h[1]);
+    if (h[0] != ULLONG_MAX)
+        return fail(c, NBODY_ENONFINITE, "non-finite state at particle %llu", h[0]);
+    if (use_nccl(c)) {
+        ncclResult_t ar;
+        CKNCCL(c, nccl().CommGetAsyncError(c->comm, &ar));
+        if (ar != ncclSuccess && ar != ncclInProgress)
+            return fail(c, NBODY_ENCCL, "NCCL async error: %s", nccl().GetErrorString(ar));
+    }
+    return NBODY_OK;
+}
+
+// copy the local [3][n_loc_pad] rows of every shard to/from a user
+// [3][k] array (k = local count, or n in loopback mode)
+int copy_rows(nbody_ctx* c, double* user, bool to_user, bool which_v, bool* host) {
+    int64_t k0 = c->sh.front().plan.i0;
+    int64_t k = c->sh.back().plan.i1 - k0;
+    *host = !is_device_ptr(user);
+    for (auto& s : c->sh) {
+        if (s.n_loc <= 0) continue;
+        double* dev = which_v ? s.v : s.x;
+        double* u = user + (s.plan.i0 - k0);
+        if (to_user)
+            CK(c, cudaMemcpy2DAsync(u, k * 8, dev, s.n_loc_pad * 8, s.n_loc * 8, 3, cudaMemcpyDefault,
+                                    c->stream));
+        else
+            CK(c, cudaMemcpy2DAsync(dev, s.n_loc_pad * 8, u, k * 8, s.n_loc * 8, 3, cudaMemcpyDefault,
+                                    c->stream));
+    }
+    return NBODY_OK;
+}
+
+void free_ctx(nbody_ctx* c) {
+    if (!c) return;
+    cudaSetDevice(c->cfg.device);
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    if (c->comm && nccl().ok) nccl().CommDestroy(c->comm);
+    for (auto& s : c->sh) {
+        cudaFree(s.m); cudaFree(s.x); cudaFree(s.v); cudaFree(s.a0); cudaFree(s.j0);
+        cudaFree(s.xp); cudaFree(s.vp); cudaFree(s.partial);
+    }
+    cudaFree(c->pkt);
+    cudaFree(c->eall);
+    cudaFree(c->eblk);
+    cudaFree(c->eout);
+    cudaFree(c->flags);
+    for (auto e : c->prof_ev) cudaEventDestroy(e);
+    if (c->ev_packed) cudaEventDestroy(c->ev_packed);
+    if (c->ev_gathered) cudaEventDestroy(c->ev_gathered);
+    if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
+    if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+    delete c;
+}
+
+template <class T>
+int dalloc(nbody_ctx* c, T** p, size_t count) {
+    if (count == 0) count = 1;
+    cudaError_t e = cudaMalloc(reinterpret_cast<void**>(p), count * sizeof(T));
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(c, NBODY_ENOMEM, "cudaMalloc of %zu bytes failed: %s", count * sizeof(T),
+                    cudaGetErrorString(e));
+    }
+    return NBODY_OK;
+}
+
+int init_impl(const nbody_config* cfg, const double* m, const double* x, const double* v,
+              nbody_ctx* c) {
+    int rc;
+    const nbody_config& k = *cfg;
+    if (!(std::isfinite(k.G) && k.G > 0)) return fail(c, NBODY_EINVAL, "G must be finite and > 0");
+    if (!(std::isfinite(k.eps) && k.eps >= 0)) return fail(c, NBODY_EINVAL, "eps must be finite and >= 0");
+    if (!(std::isfinite(k.dt) && k.dt > 0)) return fail(c, NBODY_EINVAL, "dt must be finite and > 0");
+    if (k.integrator != NBODY_HERMITE4)
+        return fail(c, NBODY_EINVAL, "integrator %d not supported", k.integrator);
+    if (!m || !x || !v) return fail(c, NBODY_EINVAL, "m, x and v must be non-NULL");
+    if (k.world > 1 && !k.loopback && !k.nccl_id)
+        return fail(c, NBODY_EINVAL, "world > 1 needs nccl_id (or loopback)");
+    c->cfg = k;
+    c->n = k.n;
+    c->eps2f = (float)(k.eps * k.eps);
+    c->nshards = k.loopback ? k.world : 1;
+    c->sh.resize(c->nshards);
+    std::string why;
+    for (int s = 0; s < c->nshards; ++s) {
+        const int32_t r = k.loopback ? s : k.rank;
+        if ((rc = make_plan(k.n, k.world, r, k.jchunks, &c->sh[s].plan, &why)))
+            return fail(c, rc, "%s", why.c_str());
+    }
+    const Plan& p0 = c->sh[0].plan;
+    c->L = std::max<int64_t>((int64_t)k.world * p0.slot, p0.n_chunks * p0.chunk);
+
+    CK(c, cudaSetDevice(k.device));
+    if (k.stream) {
+        c->stream = (cudaStream_t)k.stream;
+    } else {
+        CK(c, cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        c->own_stream = true;
+    }
+    CK(c, cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking));
+    CK(c, cudaEventCreateWithFlags(&c->ev_packed, cudaEventDisableTiming));
+    CK(c, cudaEventCreateWithFlags(&c->ev_gathered, cudaEventDisableTiming));
+
+    if ((rc = dalloc(c, &c->pkt, (size_t)c->L))) return rc;
+    if ((rc = dalloc(c, &c->flags, 4))) return rc;
+    CK(c, cudaMemsetAsync(c->flags, 0xff, 4 * sizeof(unsigned long long), c->stream));
+    CK(c, nb::launch_fill_padding(c->pkt, 0, c->L, c->stream));
+    c->n_kernels++;
+
+    const int64_t ib = nb::force_i_per_block();
+    for (auto& s : c->sh) {
+        s.n_loc = (int32_t)(s.plan.i1 - s.plan.i0);
+        s.n_loc_pad = std::max<int64_t>(ib, ib * ((s.n_loc + ib - 1) / ib));
+        const size_t v3 = 3 * (size_t)s.n_loc_pad;
+        if ((rc = dalloc(c, &s.m, (size_t)s.n_loc_pad))) return rc;
+        if ((rc = dalloc(c, &s.x, v3)) || (rc = dalloc(c, &s.v, v3)) || (rc = dalloc(c, &s.a0, v3)) ||
+            (rc = dalloc(c, &s.j0, v3)) || (rc = dalloc(c, &s.xp, v3)) || (rc = dalloc(c, &s.vp, v3)))
+            return rc;
+        if ((rc = dalloc(c, &s.partial, (size_t)s.plan.n_chunks * 6 * s.n_loc_pad))) return rc;
+        // local chunks: those inside [i0, i0 + slot) of this rank's exchange slice
+        const int64_t lo = s.plan.i0 == s.plan.i1 ? 0 : s.plan.i0;
+        const int64_t hi = s.plan.i0 == s.plan.i1 ? 0 : s.plan.i0 + s.plan.slot;
+        s.c_lo = (int32_t)((lo + s.plan.chunk - 1) / s.plan.chunk);
+        s.c_hi = (int32_t)std::min<int64_t>(s.plan.n_chunks, hi / s.plan.chunk);
+        if (s.c_hi < s.c_lo) s.c_hi = s.c_lo;
+        if (s.n_loc <= 0) continue;
+        CK(c, cudaMemcpyAsync(s.m, m + s.plan.i0, s.n_loc * 8, cudaMemcpyDefault, c->stream));
+        CK(c, cudaMemcpy2DAsync(s.x, s.n_loc_pad * 8, x + s.plan.i0, k.n * 8, s.n_loc * 8, 3,
+                                cudaMemcpyDefault, c->stream));
+        CK(c, cudaMemcpy2DAsync(s.v, s.n_loc_pad * 8, v + s.plan.i0, k.n * 8, s.n_loc * 8, 3,
+                                cudaMemcpyDefault, c->stream));
+        CK(c, nb::launch_validate(state_args(c, s), c->flags + 2, c->stream));
+        c->n_kernels++;
+    }
+    unsigned long long bad[2];
+    CK(c, cudaMemcpyAsync(bad, c->flags + 2, sizeof bad, cudaMemcpyDeviceToHost, c->stream));
+    CK(c, cudaStreamSynchronize(c->stream));
+    if (bad[0] != ULLONG_MAX) return fail(c, NBODY_EINVAL, "mass of particle %llu is not finite and > 0", bad[0]);
+    if (bad[1] != ULLONG_MAX) return fail(c, NBODY_EINVAL, "position or velocity of particle %llu is not finite", bad[1]);
+
+    if (k.nccl_id && !k.loopback) {
+        NcclApi& api = nccl();
+        if (!api.ok) return fail(c, NBODY_ENCCL, "%s", api.why.c_str());
+        ncclUniqueId id;
+        memcpy(id.internal, k.nccl_id, NCCL_UNIQUE_ID_BYTES);
+        CKNCCL(c, api.CommInitRank(&c->comm, k.world, id, k.rank));
+    }
+    return NBODY_OK;
+}
+
+}  // namespace
+
+// ======================================================================= C-ABI
+
+extern "C" {
+
+int nbody_plan(int64_t n, int32_t world, int32_t rank, int32_t jchunks, int64_t* i0, int64_t* i1,
+               int64_t* slot, int64_t* chunk, int64_t* n_chunks) {
+    Plan p;
+    std::string why;
+    int rc = make_plan(n, world, rank, jchunks, &p, &why);
+    if (rc) return fail(nullptr, rc, "%s", why.c_str());
+    if (i0) *i0 = p.i0;
+    if (i1) *i1 = p.i1;
+    if (slot) *slot = p.slot;
+    if (chunk) *chunk = p.chunk;
+    if (n_chunks) *n_chunks = p.n_chunks;
+    return NBODY_OK;
+}
+
+int nbody_nccl_unique_id(uint8_t out[128]) {
+    NcclApi& api = nccl();
+    if (!api.ok) return fail(nullptr, NBODY_ENCCL, "%s", api.why.c_str());
+    ncclUniqueId id;
+    ncclResult_t r = api.GetUniqueId(&id);
+    if (r != ncclSuccess) return fail(nullptr, NBODY_ENCCL, "ncclGetUniqueId: %s", api.GetErrorString(r));
+    memcpy(out, id.internal, NCCL_UNIQUE_ID_BYTES);
+    return NBODY_OK;
+}
+
+int nbody_init(const nbody_config* cfg, const double* m, const double* x, const double* v,
+               nbody_ctx** out) {
+    if (!out) return fail(nullptr, NBODY_EINVAL, "out is NULL");
+    *out = nullptr;
+    if (!cfg) return fail(nullptr, NBODY_EINVAL, "cfg is NULL");
+    nbody_ctx* c = new nbody_ctx();
+    int rc = init_impl(cfg, m, x, v, c);
+    if (rc) {
+        g_last_error = c->err;
+        free_ctx(c);
+        return rc;
+    }
+    *out = c;
+    return NBODY_OK;
+}
+
+int nbody_local_range(const nbody_ctx* c, int64_t* i0, int64_t* i1) {
+    if (!c) return fail(nullptr, NBODY_EINVAL, "null context");
+    if (i0) *i0 = c->sh.front().plan.i0;
+    if (i1) *i1 = c->sh.back().plan.i1;
+    return NBODY_OK;
+}
+
+int nbody_compute_forces(nbody_ctx* c, double* acc, double* jerk) {
+    GUARD(c);
+    int rc;
+    c->have_a0 = false;
+    if ((rc = ensure_forces(c))) return rc;
+    const int64_t k0 = c->sh.front().plan.i0;
+    const int64_t k = c->sh.back().plan.i1 - k0;
+    bool host = false;
+    for (auto& s : c->sh) {
+        if (s.n_loc <= 0) continue;
+        if (acc) {
+            host |= !is_device_ptr(acc);
+            CK(c, cudaMemcpy2DAsync(acc + (s.plan.i0 - k0), k * 8, s.a0, s.n_loc_pad * 8, s.n_loc * 8, 3,
+                                    cudaMemcpyDefault, c->stream));
+        }
+        if (jerk) {
+            host |= !is_device_ptr(jerk);
+            CK(c, cudaMemcpy2DAsync(jerk + (s.plan.i0 - k0), k * 8, s.j0, s.n_loc_pad * 8, s.n_loc * 8,
+                                    3, cudaMemcpyDefault, c->stream));
+        }
+    }
+    if (host) return check_flags(c);
+    return NBODY_OK;
+}
+
+int nbody_step(nbody_ctx* c, int32_t nsteps) {
+    GUARD(c);
+    if (nsteps < 1) return fail(c, NBODY_EINVAL, "nsteps must be >= 1");
+    int rc;
+    if ((rc = ensure_forces(c))) return rc;
+    if (!c->predicted) {
+        for (auto& s : c->sh) {
+            CK(c, nb::launch_predict_pack(state_args(c, s), c->stream));
+            c->n_kernels++;
+        }
+        c->predicted = true;
+    }
+    for (int32_t t = 0; t < nsteps; ++t) {
+        if ((rc = exchange_and_force(c))) return rc;
+        for (auto& s : c->sh) {
+            CK(c, nb::launch_correct_predict_pack(state_args(c, s), c->stream));
+            c->n_kernels++;
+        }
+    }
+    return NBODY_OK;
+}
+
+int nbody_energy(nbody_ctx* c, double* kinetic, double* potential) {
+    GUARD(c);
+    int rc;
+    if (!c->eall) {
+        if ((rc = dalloc(c, &c->eall, (size_t)c->L))) return rc;
+        CK(c, cudaMemsetAsync(c->eall, 0, (size_t)c->L * sizeof(double4), c->stream));
+        int mb = 1;
+        for (auto& s : c->sh) mb = std::max(mb, nb::energy_blocks(s.n_loc));
+        if ((rc = dalloc(c, &c->eblk, 2 * (size_t)mb))) return rc;
+        c->eblk_cap = mb;
+        if ((rc = dalloc(c, &c->eout, 2 * (size_t)std::max(c->nshards, (int)c->cfg.world)))) return rc;
+    }
+    for (auto& s : c->sh) {
+        CK(c, nb::launch_energy_pack(state_args(c, s), c->eall, c->stream));
+        c->n_kernels++;
+    }
+    if (use_nccl(c)) {
+        const size_t cnt = (size_t)c->sh[0].plan.slot * 4;
+        double* base = reinterpret_cast<double*>(c->eall);
+        CKNCCL(c, nccl().AllGather(base + (size_t)c->cfg.rank * cnt, base, cnt, ncclFloat64, c->comm,
+                                   c->stream));
+    }
+    const double eps2 = (double)c->eps2f;
+    for (int q = 0; q < c->nshards; ++q) {
+        Shard& s = c->sh[q];
+        const int slot = use_nccl(c) ? c->cfg.rank : q;
+        CK(c, nb::launch_energy(c->eall, c->n, s.plan.i0, s.n_loc, s.v, s.n_loc_pad, s.m, eps2, c->eblk,
+                                c->eblk_cap, c->eout + 2 * slot, c->stream));
+        c->n_kernels += 2;
+    }
+    const int nsum = use_nccl(c) ? c->cfg.world : c->nshards;
+    if (use_nccl(c)) {
+        // gather every rank's (KE, PE) pair (in place); summed on the host in rank order
+        CKNCCL(c, nccl().AllGather(c->eout + 2 * c->cfg.rank, c->eout, 2, ncclFloat64, c->comm,
+                                   c->stream));
+    }
+    std::vector<double> h(2 * (size_t)nsum);
+    CK(c, cudaMemcpyAsync(h.data(), c->eout, h.size() * 8, cudaMemcpyDeviceToHost, c->stream));
+    if ((rc = check_flags(c))) return rc;
+    double ke = 0, pe = 0;
+    for (int q = 0; q < nsum; ++q) {
+        ke += h[2 * q];
+        pe += h[2 * q + 1];
+    }
+    if (kinetic) *kinetic = ke;
+    if (potential) *potential = -0.5 * c->cfg.G * pe;
+    return NBODY_OK;
+}
+
+int nbody_get_state(nbody_ctx* c, double* x, double* v) {
+    GUARD(c);
+    int rc;
+    bool hx = false, hv = false;
+    if (x && (rc = copy_rows(c, x, true, false, &hx))) return rc;
+    if (v && (rc = copy_rows(c, v, true, true, &hv))) return rc;
+    if (hx || hv) return check_flags(c);
+    return NBODY_OK;
+}
+
+int nbody_set_state(nbody_ctx* c, const double* x, const double* v, int32_t keep_forces) {
+    GUARD(c);
+    int rc;
+    bool hx = false, hv = false;
+    if (x && (rc = copy_rows(c, const_cast<double*>(x), false, false, &hx))) return rc;
+    if (v && (rc = copy_rows(c, const_cast<double*>(v), false, true, &hv))) return rc;
+    CK(c, cudaMemsetAsync(c->flags + 2, 0xff, 2 * sizeof(unsigned long long), c->stream));
+    for (auto& s : c->sh) {
+        CK(c, nb::launch_validate(state_args(c, s), c->flags + 2, c->stream));
+        c->n_kernels++;
+    }
+    unsigned long long bad[2];
+    CK(c, cudaMemcpyAsync(bad, c->flags + 2, sizeof bad, cudaMemcpyDeviceToHost, c->stream));
+    CK(c, cudaStreamSynchronize(c->stream));
+    if (bad[1] != ULLONG_MAX) {
+        c->have_a0 = false;
+        c->predicted = false;
+        return fail(c, NBODY_EINVAL, "position or velocity of particle %llu is not finite", bad[1]);
+    }
+    if (!keep_forces) c->have_a0 = false;
+    c->predicted = false;
+    return NBODY_OK;
+}
+
+int nbody_sync(nbody_ctx* c) {
+    GUARD(c);
+    CK(c, cudaStreamSynchronize(c->comm_stream));
+    return check_flags(c);
+}
+
+int nbody_prof_enable(nbody_ctx* c, int32_t on) {
+    if (!c) return fail(nullptr, NBODY_EINVAL, "null context");
+    c->prof = on != 0;
+    return NBODY_OK;
+}
+
+int nbody_prof_read(nbody_ctx* c, double* force_ms, int64_t* force_launches, int64_t* kernel_launches,
+                    int32_t reset) {
+    GUARD(c);
+    CK(c, cudaStreamSynchronize(c->stream));
+    double ms = 0;
+    for (size_t q = 0; q + 1 < c->prof_used; q += 2) {
+        float t = 0;
+        CK(c, cudaEventElapsedTime(&t, c->prof_ev[q], c->prof_ev[q + 1]));
+        ms += t;
+    }
+    if (force_ms) *force_ms = ms;
+    if (force_launches) *force_launches = c->n_force;
+    if (kernel_launches) *kernel_launches = c->n_kernels;
+    if (reset) {
+        c->prof_used = 0;
+        c->n_force = 0;
+        c->n_kernels = 0;
+    }
+    return NBODY_OK;
+}
+
+const char* nbody_last_error(const nbody_ctx* c) {
+    if (c) return c->err.c_str();
+    return g_last_error.c_str();
+}
+
+void nbody_destroy(nbody_ctx* c) { free_ctx(c); }
+
+}  // extern "C"

@@ -1,0 +1,305 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the fp64 oracle.
+
+All inputs are seeded and synthetic (paper_2509_19294_b200.inputs) and, for
+force parity, fp32-representable (R#9), so both sides see identical values.
+Bars: max per-particle relative acceleration error 1e-5 (BASELINE.json), jerk
+1e-4 (R#12), the paper's 0.05 % / 0.2 % of the typical magnitude,
+energy drift within 2x the oracle's own drift (BASELINE.json, R#14).
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_2509_19294_b200 import binding, inputs
+from metrics import (TOL_ACC, TOL_JERK, TOL_PAPER_ACC, TOL_PAPER_JERK, max_rel,
+                     momentum_residual, paper_norm, sample_indices)
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+def eps2_of(eps):
+    return float(np.float32(eps * eps))   # R#18: both paths use fp32(eps^2)
+
+
+def gpu_forces(m, x, v, eps, **kw):
+    with binding.NBody(m, x, v, eps=eps, dt=1.0 / 1024, **kw) as sim:
+        a, j = sim.forces()
+        sim.sync()
+        return a.cpu().numpy(), j.cpu().numpy()
+
+
+def check_forces(m, x, v, eps, idx=None, **kw):
+    a, j = gpu_forces(m, x, v, eps, **kw)
+    ao, jo = oracle.forces(m, x, v, eps2_of(eps), idx=idx)
+    if idx is not None:
+        a, j = a[:, idx], j[:, idx]
+    ea, ej = max_rel(a, ao), max_rel(j, jo)
+    pa, pj = paper_norm(a, ao), paper_norm(j, jo)
+    assert ea <= TOL_ACC, ea
+    assert ej <= TOL_JERK, ej
+    assert pa <= TOL_PAPER_ACC and pj <= TOL_PAPER_JERK, (pa, pj)
+    return ea, ej
+
+
+# --------------------------------------------------------------- closed forms
+
+def test_two_body_closed_form_eps0():
+    """SPEC S:313-314 with eps = 0 (guarded j == i path): a = (+-1, 0, 0), j1 = (0, 1, 0)."""
+    m = np.array([1.0, 1.0])
+    x = np.array([[0.0, 1.0], [0.0, 0.0], [0.0, 0.0]])
+    v = np.array([[0.0, 0.0], [0.0, 1.0], [0.0, 0.0]])
+    a, j = gpu_forces(m, x, v, 0.0)
+    assert np.allclose(a, [[1, -1], [0, 0], [0, 0]], atol=1e-6, rtol=0)
+    assert np.allclose(j, [[0, 0], [1, -1], [0, 0]], atol=1e-6, rtol=0)
+
+
+def test_equilateral_triangle():
+    m = np.ones(3)
+    pts = np.array([[0.0, 1.0, 0.5], [0.0, 0.0, math.sqrt(3) / 2], [0.0, 0.0, 0.0]])
+    a, _ = gpu_forces(m, pts, np.zeros((3, 3)), 0.0)
+    assert np.allclose(np.linalg.norm(a, axis=0), math.sqrt(3), rtol=1e-6)
+
+
+# ------------------------------------------------------------ force parity
+
+@pytest.mark.parametrize("n", [2, 3, 255, 256, 257, 511, 1000, 1025, 3000, 4097])
+def test_ragged_sizes(n):
+    m, x, v = inputs.parity_round(*inputs.uniform_cube(n, 1000 + n))
+    check_forces(m, x, v, 1e-2)
+
+
+@pytest.mark.parametrize("cfg", ["C1", "C2"])
+def test_config_forces_all_particles(cfg):
+    c = inputs.CONFIGS[cfg]
+    m, x, v = inputs.make(cfg)
+    check_forces(m, x, v, c.eps)
+
+
+@pytest.mark.parametrize("cfg", ["C3", "C4", "C5"])
+def test_config_forces_sampled(cfg):
+    """Full-size configs in the bench's launch configuration, R#11 sample of i."""
+    c = inputs.CONFIGS[cfg]
+    m, x, v = inputs.make(cfg)
+    idx = sample_indices(x, n_stride=4096 if cfg == "C5" else 8192)
+    check_forces(m, x, v, c.eps, idx=idx)
+
+
+def test_two_cluster_small_all_particles():
+    m, x, v = inputs.parity_round(*inputs.two_cluster(8192, 4))
+    check_forces(m, x, v, 1e-3)
+
+
+def test_momentum_conservation_gpu():
+    m, x, v = inputs.make("C2")
+    a, j = gpu_forces(m, x, v, 1e-3)
+    assert momentum_residual(m, a) < 1e-6
+    assert momentum_residual(m, j) < 1e-5
+
+
+@pytest.mark.parametrize("jchunks", [1, 7, 128])
+def test_jchunk_counts(jchunks):
+    m, x, v = inputs.parity_round(*inputs.plummer(5000, 8))
+    check_forces(m, x, v, 1e-3, jchunks=jchunks)
+
+
+# ----------------------------------------------------- determinism / sharding
+
+def test_loopback_shards_bit_identical():
+    """Results do not depend on the number of i-shards: loopback
+    world = 2, 3, 8 (ragged, with an empty tail rank) equals world = 1 bit-for-bit."""
+    n = 20000
+    m, x, v = inputs.parity_round(*inputs.plummer(n, 21))
+    ref = None
+    for world in (1, 2, 3, 8):
+        with binding.NBody(m, x, v, eps=1e-3, dt=1 / 1024, world=world, loopback=world > 1) as s:
+            a, j = s.forces()
+            s.step(3)
+            xs, vs = s.state()
+            got = [t.cpu().numpy() for t in (a, j, xs, vs)]
+        if ref is None:
+            ref = got
+        else:
+            for g, r in zip(got, ref):
+                assert np.array_equal(g, r), world
+
+
+def test_tiny_n_many_shards():
+    m, x, v = inputs.parity_round(*inputs.uniform_cube(300, 5))
+    a1, j1 = gpu_forces(m, x, v, 1e-2)
+    a3, j3 = gpu_forces(m, x, v, 1e-2, world=3, loopback=True)   # rank 2 owns nothing
+    assert np.array_equal(a1, a3) and np.array_equal(j1, j3)
+
+
+def test_nccl_single_rank_communicator():
+    """world = 1 with an NCCL communicator exercises the exchange path on one GPU."""
+    m, x, v = inputs.make("C1")
+    ref = gpu_forces(m, x, v, 1e-2)
+    got = gpu_forces(m, x, v, 1e-2, nccl_id=binding.nccl_unique_id())
+    assert np.array_equal(ref[0], got[0]) and np.array_equal(ref[1], got[1])
+
+
+def test_repeat_runs_bit_identical():
+    m, x, v = inputs.make("C1")
+    r1 = gpu_forces(m, x, v, 1e-2)
+    r2 = gpu_forces(m, x, v, 1e-2)
+    assert np.array_equal(r1[0], r2[0]) and np.array_equal(r1[1], r2[1])
+
+
+# ------------------------------------------------------------------ energy
+
+@pytest.mark.parametrize("which", ["C1", "C2", "cluster"])
+def test_energy_matches_oracle(which):
+    if which == "cluster":
+        m, x, v = inputs.parity_round(*inputs.two_cluster(4096, 9))
+        eps = 1e-3
+    else:
+        m, x, v = inputs.make(which)
+        eps = inputs.CONFIGS[which].eps
+    with binding.NBody(m, x, v, eps=eps, dt=1 / 1024) as s:
+        ke, pe = s.energy()
+    ko, po = oracle.energy(m, x, v, eps2_of(eps))
+    assert abs(ke - ko) <= 1e-13 * abs(ko)
+    assert abs(pe - po) <= 1e-12 * abs(po)
+
+
+# ------------------------------------------------------------- trajectories
+
+def _drift(E):
+    return max(abs(e - E[0]) / abs(E[0]) for e in E)
+
+
+def run_gpu_traj(m, x, v, eps, dt, nsteps, every):
+    states = [(x, v)]
+    with binding.NBody(m, x, v, eps=eps, dt=dt) as s:
+        done = 0
+        while done < nsteps:
+            k = min(every, nsteps - done)
+            s.step(k)
+            done += k
+            xs, vs = s.state()
+            s.sync()
+            states.append((xs.cpu().numpy(), vs.cpu().numpy()))
+    return states
+
+
+def run_oracle_traj(m, x, v, eps, dt, nsteps, every):
+    states = [(x, v)]
+    acc = jerk = None
+    done = 0
+    while done < nsteps:
+        k = min(every, nsteps - done)
+        x, v, acc, jerk = oracle.hermite(m, x, v, eps2_of(eps), dt, k, acc=acc, jerk=jerk)
+        done += k
+        states.append((x, v))
+    return states
+
+
+@pytest.mark.parametrize("cfg,every,dx_tol,dv_tol", [("C1", 1, 1e-9, 1e-6), ("C2", 10, 1e-6, 1e-4)])
+def test_trajectory_and_energy_drift(cfg, every, dx_tol, dv_tol):
+    """R#14/R#15: same fp32 IC, Hermite P(EC)^1 on both sides; trajectory deltas and
+    drift D = max_k |E_k - E_0| / |E_0| with both energies from the oracle."""
+    c = inputs.CONFIGS[cfg]
+    m, x, v = inputs.make(cfg)
+    g = run_gpu_traj(m, x, v, c.eps, c.dt, c.steps, every)
+    o = run_oracle_traj(m, x, v, c.eps, c.dt, c.steps, every)
+    e2 = eps2_of(c.eps)
+    Eg = [sum(oracle.energy(m, xs, vs, e2)) for xs, vs in g]
+    Eo = [sum(oracle.energy(m, xs, vs, e2)) for xs, vs in o]
+    Dg, Do = _drift(Eg), _drift(Eo)
+    assert Dg <= 2 * max(Do, 1e-11), (Dg, Do)
+    dx = np.linalg.norm(g[-1][0] - o[-1][0], axis=0)
+    dv = np.linalg.norm(g[-1][1] - o[-1][1], axis=0)
+    assert dx.max() <= dx_tol and dv.max() <= dv_tol, (dx.max(), dv.max())
+    if cfg == "C2":
+        assert np.median(dx) <= 1e-9
+    # momentum: sum m v stays at its initial value
+    p0 = v @ m
+    p1 = g[-1][1] @ m
+    assert np.max(np.abs(p1 - p0)) < 1e-9
+
+
+def test_gpu_energy_tracks_oracle_energy_along_trajectory():
+    c = inputs.CONFIGS["C1"]
+    m, x, v = inputs.make("C1")
+    with binding.NBody(m, x, v, eps=c.eps, dt=c.dt) as s:
+        s.step(10)
+        ke, pe = s.energy()
+        xs, vs = s.state()
+    ko, po = oracle.energy(m, xs.cpu().numpy(), vs.cpu().numpy(), eps2_of(c.eps))
+    assert abs((ke + pe) - (ko + po)) <= 1e-12 * abs(ko + po)
+
+
+@pytest.mark.parametrize("e,tol", [(0.0, 1e-5), (0.5, 1e-5)])
+def test_kepler_one_period_gpu(e, tol):
+    """X7: fp32 forces, fp64 Hermite, eps = 0 guarded path; one period at dt ~ 1/1024."""
+    m, x, v = inputs.kepler(e)
+    nsteps = 6434
+    dt = 2 * math.pi / nsteps
+    with binding.NBody(m, x, v, eps=0.0, dt=dt) as s:
+        s.step(nsteps)
+        xs, _ = s.state()
+        xs = xs.cpu().numpy()
+    rel = xs[:, 1] - xs[:, 0]
+    target = np.array([1.0 - e, 0.0, 0.0])
+    assert np.linalg.norm(rel - target) < tol
+
+
+def test_state_round_trip_keeps_trajectory():
+    """set_state(get_state(), keep_forces) through host memory is transparent."""
+    m, x, v = inputs.make("C1")
+    with binding.NBody(m, x, v, eps=1e-2, dt=1 / 1024) as s:
+        s.step(4)
+        ref = [t.cpu().numpy() for t in s.state()]
+    with binding.NBody(m, x, v, eps=1e-2, dt=1 / 1024) as s:
+        s.step(2)
+        hx = np.empty((3, 1024))
+        hv = np.empty((3, 1024))
+        binding._check(binding.lib().nbody_get_state(s._ctx, hx.ctypes.data, hv.ctypes.data), s._ctx)
+        s.set_state(hx, hv, keep_forces=True)
+        s.step(2)
+        got = [t.cpu().numpy() for t in s.state()]
+    assert np.array_equal(ref[0], got[0]) and np.array_equal(ref[1], got[1])
+
+
+def test_host_pointer_inputs_and_outputs():
+    m, x, v = inputs.make("C1")
+    a_dev, j_dev = gpu_forces(m, x, v, 1e-2)
+    with binding.NBody(m, x, v, eps=1e-2, dt=1 / 1024) as s:
+        ha = np.empty((3, 1024))
+        hj = np.empty((3, 1024))
+        binding._check(binding.lib().nbody_compute_forces(s._ctx, ha.ctypes.data, hj.ctypes.data),
+                       s._ctx)
+    assert np.array_equal(ha, a_dev) and np.array_equal(hj, j_dev)
+
+
+# ------------------------------------------------------------------- errors
+
+def test_invalid_inputs_name_the_particle():
+    m, x, v = inputs.make("C1")
+    xb = x.copy()
+    xb[1, 77] = np.nan
+    with pytest.raises(binding.NBodyError, match="particle 77") as e:
+        binding.NBody(m, xb, v, eps=1e-2, dt=1 / 1024)
+    assert e.value.code == binding.NBODY_EINVAL
+    mb = m.copy()
+    mb[5] = 0.0
+    with pytest.raises(binding.NBodyError, match="particle 5"):
+        binding.NBody(mb, x, v, eps=1e-2, dt=1 / 1024)
+
+
+def test_coincident_pair_eps0_is_reported_and_sticky():
+    m = np.ones(4)
+    x = np.array([[0.0, 1.0, 1.0, 3.0], [0.0, 0.0, 0.0, 0.0], [0.0, 0.0, 0.0, 0.0]])
+    s = binding.NBody(m, x, np.zeros((3, 4)), eps=0.0, dt=1 / 1024)
+    s.forces()
+    with pytest.raises(binding.NBodyError) as e:
+        s.sync()
+    assert e.value.code == binding.NBODY_ENONFINITE and "coincident" in str(e.value)
+    with pytest.raises(binding.NBodyError) as e2:
+        s.step(1)
+    assert e2.value.code == binding.NBODY_ESTATE
+    s.close()
