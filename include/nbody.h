@@ -92,7 +92,9 @@ typedef struct {
                              world == 1 (then a 1-rank NCCL communicator is
                              used for the exchange).                           */
     void* stream;         /* cudaStream_t to order work on; NULL -> the library
-                             creates a non-blocking stream                      */
+                             creates a non-blocking stream; pass
+                             cudaStreamLegacy ((void*)1) for the legacy
+                             default stream                                    */
 } nbody_config;
 
 /* Partition and reduction plan (pure host function, no GPU needed).

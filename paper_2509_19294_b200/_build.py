@@ -62,20 +62,25 @@ def nvcc() -> str:
     return p
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not stale():
+def build(force: bool = False, verbose: bool = False, defines=(), out: str | None = None) -> str:
+    """Compile every csrc/*.cu into one shared library (default: the in-tree LIB).
+
+    `defines` (e.g. ["FK_PAIRS=3"]) and `out` build tuning variants elsewhere
+    (scripts/sweep_force.py); the product library is always the default."""
+    target = out or LIB
+    if not force and not defines and out is None and not stale():
         return LIB
-    tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [nvcc(), *NVCC_FLAGS, "-I", INCLUDE, "-I", CSRC, "-I", nccl_include(),
-           "-o", tmp, *sources(), "-ldl"]
+    tmp = target + f".tmp{os.getpid()}"
+    cmd = [nvcc(), *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-I", INCLUDE, "-I", CSRC,
+           "-I", nccl_include(), "-o", tmp, *sources(), "-ldl"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if verbose or r.returncode:
         print(r.stdout)
         print(r.stderr)
     if r.returncode:
         raise RuntimeError(f"nvcc failed ({r.returncode})")
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, target)
+    return target
 
 
 if __name__ == "__main__":

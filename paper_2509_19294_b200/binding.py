@@ -68,7 +68,9 @@ def lib():
     global _lib
     if _lib is not None:
         return _lib
-    path = _build.build() if _build.stale() else _build.LIB
+    path = os.environ.get("NBODY_LIB")    # tuning sweeps only (scripts/sweep_force.py)
+    if not path:
+        path = _build.build() if _build.stale() else _build.LIB
     _set_nccl_path()
     L = ctypes.CDLL(path)
     i32, i64, p, d = ctypes.c_int32, ctypes.c_int64, ctypes.c_void_p, ctypes.c_double
@@ -152,6 +154,8 @@ class NBody:
             stream = torch.cuda.current_stream(device)
         self.stream = stream
         raw_stream = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+        if raw_stream == 0:
+            raw_stream = 1   # cudaStreamLegacy: torch's default stream, not "library-created"
         self._keep = []
         m, x, v = (self._prep(a) for a in (m, x, v))
         n = int(m.shape[0])

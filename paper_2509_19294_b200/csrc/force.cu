@@ -28,12 +28,35 @@ namespace nb {
 
 namespace {
 
-constexpr int kThreads = 128;
-constexpr int kPairs = 2;                 // i-pairs per thread (4 i)
-constexpr int kStages = 2;                // smem ring depth (tiles)
+// Tuning knobs (defaults chosen by the sweep in scripts/sweep_force.py;
+// profiles/ holds the measurements).
+#ifndef FK_THREADS
+#define FK_THREADS 128
+#endif
+#ifndef FK_PAIRS
+#define FK_PAIRS 4
+#endif
+#ifndef FK_STAGES
+#define FK_STAGES 2
+#endif
+#ifndef FK_MINB
+#define FK_MINB 2
+#endif
+#ifndef FK_UNROLL
+#define FK_UNROLL 2
+#endif
+#ifndef FK_ACC_SMEM
+#define FK_ACC_SMEM 1
+#endif
+
+constexpr int kThreads = FK_THREADS;
+constexpr int kPairs = FK_PAIRS;          // i-pairs per thread (2 * kPairs i)
+constexpr int kStages = FK_STAGES;        // smem ring depth (tiles)
+constexpr int kUnroll = FK_UNROLL;
 constexpr int kIPerBlock = 2 * kPairs * kThreads;
 constexpr int kTileBytes = kTile * (int)sizeof(JPkt);
-constexpr int kSmemBytes = kStages * kTileBytes + 64;
+constexpr int kAccSmemBytes = FK_ACC_SMEM ? 6 * 2 * kPairs * kThreads * 8 : 0;
+constexpr int kSmemBytes = kStages * kTileBytes + 64 + kAccSmemBytes;
 
 typedef unsigned long long f2;  // packed {lo, hi} fp32 pair in one 64-bit register
 
@@ -102,7 +125,7 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t
 }
 
 template <bool kGuard>
-__global__ void __launch_bounds__(kThreads, 3) force_kernel(ForceArgs a) {
+__global__ void __launch_bounds__(kThreads, FK_MINB) force_kernel(ForceArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
     JPkt* ring = reinterpret_cast<JPkt*>(smem);
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kTileBytes);
@@ -123,8 +146,9 @@ __global__ void __launch_bounds__(kThreads, 3) force_kernel(ForceArgs a) {
             const int il = ib + (2 * p + h) * kThreads + tid;
             if (il < a.n_loc) {
                 const JPkt pk = a.pkt[a.i_base + il];
-                q[h][0] = -pk.p.x; q[h][1] = -pk.p.y; q[h][2] = -pk.p.z;
-                q[h][3] = -pk.v.x; q[h][4] = -pk.v.y; q[h][5] = -pk.v.z;
+                const float4 P = jpkt_pos(pk), V = jpkt_vel(pk);
+                q[h][0] = -P.x; q[h][1] = -P.y; q[h][2] = -P.z;
+                q[h][3] = -V.x; q[h][4] = -V.y; q[h][5] = -V.z;
             } else {  // padding i: computed, never stored
                 q[h][0] = q[h][1] = q[h][2] = 0.f;
                 q[h][3] = q[h][4] = q[h][5] = 0.f;
@@ -138,11 +162,18 @@ __global__ void __launch_bounds__(kThreads, 3) force_kernel(ForceArgs a) {
         nvz[p] = f2make(q[0][5], q[1][5]);
     }
 
+#if FK_ACC_SMEM
+    // fp64 chunk accumulators in shared memory: [k][l][tid], conflict-free
+    double* acc_s = reinterpret_cast<double*>(smem + kStages * kTileBytes + 64);
+#define ACC64(k, l) acc_s[((k) * 2 * kPairs + (l)) * kThreads + tid]
+#else
     double acc64[6][2 * kPairs];
+#define ACC64(k, l) acc64[k][l]
+#endif
 #pragma unroll
     for (int k = 0; k < 6; ++k)
 #pragma unroll
-        for (int l = 0; l < 2 * kPairs; ++l) acc64[k][l] = 0.0;
+        for (int l = 0; l < 2 * kPairs; ++l) ACC64(k, l) = 0.0;
 
     if (tid == 0) {
 #pragma unroll
@@ -157,7 +188,6 @@ __global__ void __launch_bounds__(kThreads, 3) force_kernel(ForceArgs a) {
         }
     }
 
-    const f2 eps2 = f2bc(a.eps2);
     const f2 m3 = f2bc(-3.0f);
 
     for (int t = 0; t < ntile; ++t) {
@@ -169,12 +199,25 @@ __global__ void __launch_bounds__(kThreads, 3) force_kernel(ForceArgs a) {
 #pragma unroll
         for (int p = 0; p < kPairs; ++p) ax[p] = ay[p] = az[p] = jx[p] = jy[p] = jz[p] = 0ull;
 
-#pragma unroll 4
+#pragma unroll kUnroll
         for (int jj = 0; jj < kTile; ++jj) {
-            const float4 P = tile[jj].p;
-            const float4 V = tile[jj].v;
+            const int jl = jj;
+#if NB_PKT_DUP
+            // j operands arrive as {v, v} register pairs (packet layout, internal.h)
+            const ulonglong2 A = *reinterpret_cast<const ulonglong2*>(&tile[jl].a);
+            const ulonglong2 B = *reinterpret_cast<const ulonglong2*>(&tile[jl].b);
+            const ulonglong2 C = *reinterpret_cast<const ulonglong2*>(&tile[jl].c);
+            const ulonglong2 D = *reinterpret_cast<const ulonglong2*>(&tile[jl].d);
+            const f2 xj = A.x, yj = A.y, zj = B.x, mj = B.y;
+            const f2 vxj = C.x, vyj = C.y, vzj = D.x, eps2 = D.y;
+            const float jmass = tile[jl].b.z;
+#else
+            const float4 P = tile[jl].p;
+            const float4 V = tile[jl].v;
             const f2 xj = f2bc(P.x), yj = f2bc(P.y), zj = f2bc(P.z), mj = f2bc(P.w);
-            const f2 vxj = f2bc(V.x), vyj = f2bc(V.y), vzj = f2bc(V.z);
+            const f2 vxj = f2bc(V.x), vyj = f2bc(V.y), vzj = f2bc(V.z), eps2 = f2bc(V.w);
+            const float jmass = P.w;
+#endif
 #pragma unroll
             for (int p = 0; p < kPairs; ++p) {
                 const f2 dx = fadd2(xj, nx[p]);
@@ -194,14 +237,14 @@ __global__ void __launch_bounds__(kThreads, 3) force_kernel(ForceArgs a) {
                         r_lo = 0.f;
                         const int64_t ig = a.i_base + ib + (2 * p) * kThreads + tid;
                         const int64_t jg = jc0 + (int64_t)t * kTile + jj;
-                        if (ig != jg && ig < a.i_base + a.n_loc && P.w != 0.f)
+                        if (ig != jg && ig < a.i_base + a.n_loc && jmass != 0.f)
                             atomicMin(a.coincident, (unsigned long long)ig);
                     }
                     if (s_hi == 0.f) {
                         r_hi = 0.f;
                         const int64_t ig = a.i_base + ib + (2 * p + 1) * kThreads + tid;
                         const int64_t jg = jc0 + (int64_t)t * kTile + jj;
-                        if (ig != jg && ig < a.i_base + a.n_loc && P.w != 0.f)
+                        if (ig != jg && ig < a.i_base + a.n_loc && jmass != 0.f)
                             atomicMin(a.coincident, (unsigned long long)ig);
                     }
                 }
@@ -224,12 +267,12 @@ __global__ void __launch_bounds__(kThreads, 3) force_kernel(ForceArgs a) {
 #pragma unroll
         for (int p = 0; p < kPairs; ++p) {
             float lo, hi;
-            f2split(ax[p], lo, hi); acc64[0][2 * p] += (double)lo; acc64[0][2 * p + 1] += (double)hi;
-            f2split(ay[p], lo, hi); acc64[1][2 * p] += (double)lo; acc64[1][2 * p + 1] += (double)hi;
-            f2split(az[p], lo, hi); acc64[2][2 * p] += (double)lo; acc64[2][2 * p + 1] += (double)hi;
-            f2split(jx[p], lo, hi); acc64[3][2 * p] += (double)lo; acc64[3][2 * p + 1] += (double)hi;
-            f2split(jy[p], lo, hi); acc64[4][2 * p] += (double)lo; acc64[4][2 * p + 1] += (double)hi;
-            f2split(jz[p], lo, hi); acc64[5][2 * p] += (double)lo; acc64[5][2 * p + 1] += (double)hi;
+            f2split(ax[p], lo, hi); ACC64(0, 2 * p) += (double)lo; ACC64(0, 2 * p + 1) += (double)hi;
+            f2split(ay[p], lo, hi); ACC64(1, 2 * p) += (double)lo; ACC64(1, 2 * p + 1) += (double)hi;
+            f2split(az[p], lo, hi); ACC64(2, 2 * p) += (double)lo; ACC64(2, 2 * p + 1) += (double)hi;
+            f2split(jx[p], lo, hi); ACC64(3, 2 * p) += (double)lo; ACC64(3, 2 * p + 1) += (double)hi;
+            f2split(jy[p], lo, hi); ACC64(4, 2 * p) += (double)lo; ACC64(4, 2 * p + 1) += (double)hi;
+            f2split(jz[p], lo, hi); ACC64(5, 2 * p) += (double)lo; ACC64(5, 2 * p + 1) += (double)hi;
         }
         __syncthreads();  // every warp is done reading stage s
         if (tid == 0 && t + kStages < ntile) {
@@ -246,7 +289,7 @@ __global__ void __launch_bounds__(kThreads, 3) force_kernel(ForceArgs a) {
         const int il = ib + l * kThreads + tid;
         if (il < a.n_loc) {
 #pragma unroll
-            for (int k = 0; k < 6; ++k) out[(int64_t)k * a.n_loc_pad + il] = acc64[k][l];
+            for (int k = 0; k < 6; ++k) out[(int64_t)k * a.n_loc_pad + il] = ACC64(k, l);
         }
     }
 }
@@ -258,6 +301,12 @@ int force_i_per_block() { return kIPerBlock; }
 cudaError_t launch_force(const ForceArgs& a, bool guard_self, cudaStream_t s) {
     if (a.c_count <= 0 || a.n_loc <= 0) return cudaSuccess;
     dim3 grid((unsigned)((a.n_loc + kIPerBlock - 1) / kIPerBlock), (unsigned)a.c_count);
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaFuncSetAttribute(force_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+        cudaFuncSetAttribute(force_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+        attr_set = true;
+    }
     if (guard_self)
         force_kernel<true><<<grid, kThreads, kSmemBytes, s>>>(a);
     else

@@ -31,13 +31,12 @@ __device__ __forceinline__ void flag_bad(unsigned long long* bad, int64_t ig) {
 }
 
 __device__ __forceinline__ void store_packet(JPkt* dst, const double x[3], const double v[3],
-                                             double gm) {
-    JPkt pk;
-    pk.p = make_float4(__double2float_rn(x[0]), __double2float_rn(x[1]),
-                       __double2float_rn(x[2]), __double2float_rn(gm));
-    pk.v = make_float4(__double2float_rn(v[0]), __double2float_rn(v[1]),
-                       __double2float_rn(v[2]), 0.f);
-    *dst = pk;
+                                             double gm, float eps2) {
+    const float px = __double2float_rn(x[0]), py = __double2float_rn(x[1]);
+    const float pz = __double2float_rn(x[2]), pm = __double2float_rn(gm);
+    const float qx = __double2float_rn(v[0]), qy = __double2float_rn(v[1]);
+    const float qz = __double2float_rn(v[2]);
+    *dst = make_jpkt(px, py, pz, pm, qx, qy, qz, eps2);
 }
 
 __global__ void pack_state_kernel(StateArgs a) {
@@ -47,7 +46,7 @@ __global__ void pack_state_kernel(StateArgs a) {
             x[c] = a.x[c * a.n_loc_pad + i];
             v[c] = a.v[c * a.n_loc_pad + i];
         }
-        store_packet(a.pkt + a.i_base + i, x, v, a.G * a.m[i]);
+        store_packet(a.pkt + a.i_base + i, x, v, a.G * a.m[i], a.eps2);
     }
 }
 
@@ -65,7 +64,7 @@ __device__ __forceinline__ void predict(const StateArgs& a, int i, const double 
         ok = ok && isfinite(xp[c]) && isfinite(vp[c]);
     }
     if (!ok) flag_bad(a.bad, a.i_base + i);
-    store_packet(a.pkt + a.i_base + i, xp, vp, a.G * a.m[i]);
+    store_packet(a.pkt + a.i_base + i, xp, vp, a.G * a.m[i], a.eps2);
 }
 
 __global__ void predict_pack_kernel(StateArgs a) {
@@ -128,14 +127,11 @@ __global__ void correct_predict_pack_kernel(StateArgs a) {
     }
 }
 
-__global__ void fill_padding_kernel(JPkt* pkt, int64_t from, int64_t to) {
+__global__ void fill_padding_kernel(JPkt* pkt, int64_t from, int64_t to, float eps2) {
     for (int64_t k = from + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < to;
          k += (int64_t)gridDim.x * blockDim.x) {
-        JPkt pk;
         // zero mass far away: contributes exactly 0 (padding)
-        pk.p = make_float4(1e18f, 1e18f, 1e18f, 0.f);
-        pk.v = make_float4(0.f, 0.f, 0.f, 0.f);
-        pkt[k] = pk;
+        pkt[k] = make_jpkt(1e18f, 1e18f, 1e18f, 0.f, 0.f, 0.f, 0.f, eps2);
     }
 }
 
@@ -183,9 +179,9 @@ cudaError_t launch_correct_predict_pack(const StateArgs& a, cudaStream_t s) {
     correct_predict_pack_kernel<<<grid_for(a.n_loc), kBlock, 0, s>>>(a);
     return cudaGetLastError();
 }
-cudaError_t launch_fill_padding(JPkt* pkt, int64_t from, int64_t to, cudaStream_t s) {
+cudaError_t launch_fill_padding(JPkt* pkt, int64_t from, int64_t to, float eps2, cudaStream_t s) {
     if (to <= from) return cudaSuccess;
-    fill_padding_kernel<<<grid_for(to - from), kBlock, 0, s>>>(pkt, from, to);
+    fill_padding_kernel<<<grid_for(to - from), kBlock, 0, s>>>(pkt, from, to, eps2);
     return cudaGetLastError();
 }
 

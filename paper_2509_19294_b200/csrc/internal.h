@@ -6,12 +6,49 @@
 
 namespace nb {
 
-// j-particle packet, 32 B, the B200 replacement of the paper's replicated
-// 32x32 tiles: one float4 position + G*m, one float4 velocity.
+// j-particle packet, the B200 replacement of the paper's replicated 32x32
+// tiles.  Two layouts (compile-time NB_PKT_DUP):
+//  1: 64 B, every scalar stored twice so the force loop reads each j operand
+//     as a {lo, hi} register pair (FFMA2/FADD2/FMUL2 with a broadcast .F32
+//     scalar operand run ~30% slower in isolation, scripts/ubench_fp32.cu);
+//  0: 32 B, (x, y, z, G m) (vx, vy, vz, eps2); j operands broadcast.
+// The spare lane carries the softening eps2 = fp32(eps^2).
+#ifndef NB_PKT_DUP
+#define NB_PKT_DUP 0
+#endif
+#if NB_PKT_DUP
 struct __align__(16) JPkt {
-    float4 p;  // x, y, z, G*m      (fp32, RNE from fp64 state)
-    float4 v;  // vx, vy, vz, 0
+    float4 a;  // x, x, y, y        (fp32, RNE from fp64 state)
+    float4 b;  // z, z, Gm, Gm
+    float4 c;  // vx, vx, vy, vy
+    float4 d;  // vz, vz, eps2, eps2
 };
+__device__ __forceinline__ JPkt make_jpkt(float x, float y, float z, float gm, float vx, float vy,
+                                          float vz, float eps2) {
+    JPkt k;
+    k.a = make_float4(x, x, y, y);
+    k.b = make_float4(z, z, gm, gm);
+    k.c = make_float4(vx, vx, vy, vy);
+    k.d = make_float4(vz, vz, eps2, eps2);
+    return k;
+}
+__device__ __forceinline__ float4 jpkt_pos(const JPkt& k) { return make_float4(k.a.x, k.a.z, k.b.x, k.b.z); }
+__device__ __forceinline__ float4 jpkt_vel(const JPkt& k) { return make_float4(k.c.x, k.c.z, k.d.x, k.d.z); }
+#else
+struct __align__(16) JPkt {
+    float4 p;  // x, y, z, G m      (fp32, RNE from fp64 state)
+    float4 v;  // vx, vy, vz, eps2
+};
+__device__ __forceinline__ JPkt make_jpkt(float x, float y, float z, float gm, float vx, float vy,
+                                          float vz, float eps2) {
+    JPkt k;
+    k.p = make_float4(x, y, z, gm);
+    k.v = make_float4(vx, vy, vz, eps2);
+    return k;
+}
+__device__ __forceinline__ float4 jpkt_pos(const JPkt& k) { return k.p; }   // w = G m
+__device__ __forceinline__ float4 jpkt_vel(const JPkt& k) { return k.v; }   // w = eps2
+#endif
 
 constexpr int kTile = 256;  // j per fp32 partial-sum tile (R#10)
 
@@ -41,6 +78,7 @@ struct StateArgs {
     int64_t n_loc_pad;   // row stride of x, v, a0, j0, xp, vp, partial
     int64_t i_base;      // global index of local particle 0
     double G, dt;
+    float eps2;          // fp32(eps^2), written into the packets' spare lanes
     const double* m;     // [n_loc]
     double *x, *v, *a0, *j0, *xp, *vp;  // [3][n_loc_pad]
     const double* partial;  // [n_chunks][6][n_loc_pad]
@@ -52,7 +90,7 @@ cudaError_t launch_pack_state(const StateArgs& a, cudaStream_t s);     // x, v -
 cudaError_t launch_predict_pack(const StateArgs& a, cudaStream_t s);   // x,v,a0,j0 -> xp,vp,pkt
 cudaError_t launch_fold_forces(const StateArgs& a, cudaStream_t s);    // partial -> a0, j0
 cudaError_t launch_correct_predict_pack(const StateArgs& a, cudaStream_t s);
-cudaError_t launch_fill_padding(JPkt* pkt, int64_t from, int64_t to, cudaStream_t s);
+cudaError_t launch_fill_padding(JPkt* pkt, int64_t from, int64_t to, float eps2, cudaStream_t s);
 // bad2[0]: min global index with m not finite or <= 0; bad2[1]: x or v not finite
 cudaError_t launch_validate(const StateArgs& a, unsigned long long* bad2, cudaStream_t s);
 

@@ -191,6 +191,7 @@ nb::StateArgs state_args(nbody_ctx* c, Shard& s) {
     a.i_base = s.plan.i0;
     a.G = c->cfg.G;
     a.dt = c->cfg.dt;
+    a.eps2 = c->eps2f;
     a.m = s.m;
     a.x = s.x; a.v = s.v; a.a0 = s.a0; a.j0 = s.j0; a.xp = s.xp; a.vp = s.vp;
     a.partial = s.partial;
@@ -247,7 +248,7 @@ int exchange_and_force(nbody_ctx* c) {
         CK(c, cudaEventRecord(c->ev_packed, c->stream));
         CK(c, cudaStreamWaitEvent(c->comm_stream, c->ev_packed, 0));
         float* base = reinterpret_cast<float*>(c->pkt);
-        const size_t cnt = (size_t)s.plan.slot * 8;
+        const size_t cnt = (size_t)s.plan.slot * (sizeof(JPkt) / sizeof(float));
         CKNCCL(c, nccl().AllGather(base + (size_t)c->cfg.rank * cnt, base, cnt, ncclFloat32, c->comm,
                                    c->comm_stream));
         CK(c, cudaEventRecord(c->ev_gathered, c->comm_stream));
@@ -391,7 +392,7 @@ int init_impl(const nbody_config* cfg, const double* m, const double* x, const d
     if ((rc = dalloc(c, &c->pkt, (size_t)c->L))) return rc;
     if ((rc = dalloc(c, &c->flags, 4))) return rc;
     CK(c, cudaMemsetAsync(c->flags, 0xff, 4 * sizeof(unsigned long long), c->stream));
-    CK(c, nb::launch_fill_padding(c->pkt, 0, c->L, c->stream));
+    CK(c, nb::launch_fill_padding(c->pkt, 0, c->L, c->eps2f, c->stream));
     c->n_kernels++;
 
     const int64_t ib = nb::force_i_per_block();

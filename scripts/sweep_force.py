@@ -1,0 +1,104 @@
+#!/usr/bin/env python
+"""Force-kernel tuning sweep.  `build` (CPU): compile variants into scripts/sweep/;
+`run` (GPU): time each variant's force pass at a config in a subprocess.
+
+  python scripts/sweep_force.py build
+  python scripts/sweep_force.py run [--config C4] [--reps 3]
+"""
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+OUT = os.path.join(ROOT, "scripts", "sweep")
+
+VARIANTS = {}
+for dup in (0, 1):
+    for name, d in {
+        "base":   dict(FK_THREADS=128, FK_PAIRS=2, FK_MINB=3, FK_UNROLL=4, FK_ACC_SMEM=0),
+        "u2":     dict(FK_THREADS=128, FK_PAIRS=2, FK_MINB=3, FK_UNROLL=2, FK_ACC_SMEM=0),
+        "p4s":    dict(FK_THREADS=128, FK_PAIRS=4, FK_MINB=2, FK_UNROLL=2, FK_ACC_SMEM=1),
+        "p4sU1":  dict(FK_THREADS=128, FK_PAIRS=4, FK_MINB=2, FK_UNROLL=1, FK_ACC_SMEM=1),
+        "p4b2":   dict(FK_THREADS=128, FK_PAIRS=4, FK_MINB=2, FK_UNROLL=2, FK_ACC_SMEM=0),
+        "p3s":    dict(FK_THREADS=128, FK_PAIRS=3, FK_MINB=3, FK_UNROLL=2, FK_ACC_SMEM=1),
+        "p3sb2":  dict(FK_THREADS=128, FK_PAIRS=3, FK_MINB=2, FK_UNROLL=4, FK_ACC_SMEM=1),
+        "p5s":    dict(FK_THREADS=128, FK_PAIRS=5, FK_MINB=2, FK_UNROLL=1, FK_ACC_SMEM=1),
+        "p6sT64": dict(FK_THREADS=64, FK_PAIRS=6, FK_MINB=4, FK_UNROLL=1, FK_ACC_SMEM=1),
+    }.items():
+        VARIANTS[f"d{dup}_{name}"] = dict(d, NB_PKT_DUP=dup)
+if os.environ.get("SWEEP_ONLY"):
+    VARIANTS = {k: v for k, v in VARIANTS.items() if k in os.environ["SWEEP_ONLY"].split(",")}
+
+
+def build():
+    from concurrent.futures import ThreadPoolExecutor
+    from paper_2509_19294_b200 import _build
+    os.makedirs(OUT, exist_ok=True)
+
+    def one(item):
+        name, d = item
+        path = os.path.join(OUT, f"lib_{name}.so")
+        try:
+            _build.build(defines=[f"{k}={v}" for k, v in d.items()], out=path)
+            r = subprocess.run(["cuobjdump", "-res-usage", path], capture_output=True, text=True).stdout
+            regs = [ln for ln in r.splitlines() if "force_kernelILb0" in ln]
+            return name, "ok", regs
+        except Exception as e:  # noqa: BLE001
+            return name, f"FAILED {e}", []
+    with ThreadPoolExecutor(4) as ex:
+        for name, st, regs in ex.map(one, VARIANTS.items()):
+            print(name, st)
+
+
+def time_one(config, reps):
+    import numpy as np
+    import torch
+    from paper_2509_19294_b200 import binding, inputs
+    c = inputs.CONFIGS[config]
+    m, x, v = inputs.make(config)
+    dev = torch.device("cuda", 0)
+    sim = binding.NBody(torch.from_numpy(m).to(dev), torch.from_numpy(x).to(dev),
+                        torch.from_numpy(v).to(dev), eps=c.eps, dt=c.dt)
+    sim.forces()
+    sim.sync()
+    sim.prof_enable(True)
+    sim.prof_read(reset=True)
+    for _ in range(reps):
+        sim.forces()
+    ms, nf, _ = sim.prof_read(reset=True)
+    a, j = sim.forces()
+    sim.sync()
+    chk = float(a.abs().sum().item() + j.abs().sum().item())
+    t = ms / max(nf, 1)
+    return {"ms": t, "interactions_per_s": c.n * c.n / (t * 1e-3),
+            "tflops40": 40 * c.n * c.n / (t * 1e-3) / 1e12, "checksum": chk}
+
+
+def run(config, reps):
+    for name in VARIANTS:
+        path = os.path.join(OUT, f"lib_{name}.so")
+        if not os.path.exists(path):
+            continue
+        env = dict(os.environ, NBODY_LIB=path)
+        r = subprocess.run([sys.executable, __file__, "one", config, str(reps)], env=env,
+                           capture_output=True, text=True, timeout=600)
+        line = r.stdout.strip().splitlines()[-1] if r.stdout.strip() else r.stderr[-400:]
+        print(json.dumps({"variant": name, **VARIANTS[name], "result": line}), flush=True)
+
+
+if __name__ == "__main__":
+    cmd = sys.argv[1]
+    if cmd == "build":
+        build()
+    elif cmd == "one":
+        print(json.dumps(time_one(sys.argv[2], int(sys.argv[3]))))
+    elif cmd == "run":
+        cfg = "C4"
+        reps = 3
+        if "--config" in sys.argv:
+            cfg = sys.argv[sys.argv.index("--config") + 1]
+        if "--reps" in sys.argv:
+            reps = int(sys.argv[sys.argv.index("--reps") + 1])
+        run(cfg, reps)
