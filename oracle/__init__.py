@@ -58,6 +58,8 @@ def _load():
     lib.oracle_energy.restype = ctypes.c_int
     lib.oracle_hermite.argtypes = [i64, d, d, d, i64, p, p, p, p, p, ctypes.c_int]
     lib.oracle_hermite.restype = ctypes.c_int
+    lib.oracle_leapfrog.argtypes = [i64, d, d, d, i64, p, p, p, p, ctypes.c_int]
+    lib.oracle_leapfrog.restype = ctypes.c_int
     lib.oracle_threads.argtypes = []
     lib.oracle_threads.restype = ctypes.c_int
     lib.oracle_set_threads.argtypes = [ctypes.c_int]
@@ -155,3 +157,23 @@ def hermite(m, x, v, eps2: float, dt: float, nsteps: int, G: float = 1.0,
     if rc:
         raise OracleError(f"oracle_hermite failed rc={rc}")
     return x, v, acc, jerk
+
+
+def leapfrog(m, x, v, eps2: float, dt: float, nsteps: int, G: float = 1.0, acc=None):
+    """Advance (x, v) by nsteps kick-drift-kick steps.
+
+    Returns (x, v, acc) with acc = a(x) at the final state.
+    """
+    m = _f64(m)
+    n = m.shape[0]
+    x = _f64(x, (3, n)).copy()
+    v = _f64(v, (3, n)).copy()
+    init = acc is None
+    acc = np.zeros((3, n)) if init else _f64(acc, (3, n)).copy()
+    rc = _load().oracle_leapfrog(n, float(G), float(eps2), float(dt), int(nsteps),
+                                 _ptr(m), _ptr(x), _ptr(v), _ptr(acc), 1 if init else 0)
+    if rc == 1:
+        raise OracleError("coincident pair with eps = 0")
+    if rc:
+        raise OracleError(f"oracle_leapfrog failed rc={rc}")
+    return x, v, acc

@@ -21,6 +21,9 @@
  *   - hermite: the fp64 "remaining calculations" of P:158 [Sec. 3], read
  *     as the 4th-order Hermite predictor-corrector P(EC)^1 with shared dt
  *     and the Makino-Aarseth a2/a3 corrector (R#3).
+ *   - leapfrog: kick-drift-kick (velocity Verlet) with shared dt on the
+ *     accelerations alone -- SURVEY 8(f) row f1 (the "kick-drift update"
+ *     alternative BASELINE.json names).
  *   - energy: KE = 1/2 sum m |v|^2, PE = -G sum_{i<j} m_i m_j /
  *     sqrt(r^2 + eps^2) (R#1, R#14), fp64.
  *
@@ -230,5 +233,37 @@ int oracle_hermite(int64_t n, double G, double eps2, double dt, int64_t nsteps,
     }
 done:
     free(xp); free(vp); free(a1); free(j1);
+    return rc;
+}
+
+/*
+ * oracle_leapfrog: nsteps kick-drift-kick steps (velocity Verlet), shared dt.
+ * acc [3][n] in/out holds a(x) at the current state (computed first when
+ * init_a != 0).  Per step, per particle and component:
+ *   v_half = v + a dt/2 ;  x = x + v_half dt ;  a = a(x) ;  v = v_half + a dt/2
+ * Returns 0, 1 on a coincident pair, 2 on allocation failure, 3 non-finite.
+ */
+int oracle_leapfrog(int64_t n, double G, double eps2, double dt, int64_t nsteps,
+                    const double* m, double* x, double* v, double* acc, int init_a) {
+    double* jerk = (double*)malloc(sizeof(double) * 3 * (size_t)n);
+    int rc = 0;
+    if (!jerk) return 2;
+    if (init_a && oracle_forces(n, G, eps2, m, x, v, NULL, n, acc, jerk, NULL)) {
+        rc = 1; goto done;
+    }
+    for (int64_t s = 0; s < nsteps; ++s) {
+        for (int64_t k = 0; k < 3 * n; ++k) {
+            v[k] = v[k] + acc[k] * dt / 2.0;   /* kick */
+            x[k] = x[k] + v[k] * dt;           /* drift */
+        }
+        if (oracle_forces(n, G, eps2, m, x, v, NULL, n, acc, jerk, NULL)) { rc = 1; goto done; }
+        for (int64_t k = 0; k < 3 * n; ++k) {
+            v[k] = v[k] + acc[k] * dt / 2.0;   /* kick */
+            if (!isfinite(x[k]) || !isfinite(v[k])) rc = 3;
+        }
+        if (rc) goto done;
+    }
+done:
+    free(jerk);
     return rc;
 }

@@ -322,3 +322,55 @@ def test_hermite_local_error_orders(e, t0):
     ex2, ev2 = step_err(1 / 32)
     assert 50 <= ex1 / ex2 <= 80, ex1 / ex2
     assert 26 <= ev1 / ev2 <= 38, ev1 / ev2
+
+
+# ------------------------------------------------------- leapfrog (NEXT f1)
+
+def _kepler_lf_err(e, nsteps):
+    m, x, v = inputs.kepler(e)
+    dt = 2 * math.pi / nsteps
+    x1, v1, _ = oracle.leapfrog(m, x, v, 0.0, dt, nsteps)
+    rel = x1[:, 1] - x1[:, 0]
+    return np.linalg.norm(rel - _kepler_rel(e, nsteps * dt)), (m, x, v, x1, v1)
+
+
+def test_leapfrog_second_order_convergence():
+    """KDK is 2nd order: halving dt divides the one-period Kepler error by ~4."""
+    for e in (0.0, 0.5):
+        e1, _ = _kepler_lf_err(e, 2000)
+        e2, _ = _kepler_lf_err(e, 4000)
+        assert 3.5 <= e1 / e2 <= 4.5, (e, e1, e2)
+
+
+def test_leapfrog_time_reversible():
+    """KDK is time-symmetric: n steps with +dt then n with -dt return to the start."""
+    m, x, v = inputs.make("C1")
+    x1, v1, a1 = oracle.leapfrog(m, x, v, 1e-4, 1 / 512, 20)
+    x2, v2, _ = oracle.leapfrog(m, x1, v1, 1e-4, -1 / 512, 20, acc=a1)
+    assert np.max(np.abs(x2 - x)) < 1e-12 and np.max(np.abs(v2 - v)) < 1e-11
+
+
+def test_leapfrog_local_error_order():
+    """One KDK step from an exact Kepler state: local position error O(dt^3) (ratio 8)."""
+    def err(dt):
+        r, w = _kepler_state(0.5, 1.0)
+        m = np.array([0.5, 0.5])
+        x = np.stack([-r / 2, r / 2], 1)
+        v = np.stack([-w / 2, w / 2], 1)
+        x1, _, _ = oracle.leapfrog(m, x, v, 0.0, dt, 1)
+        r1, _ = _kepler_state(0.5, 1.0 + dt)
+        return np.linalg.norm((x1[:, 1] - x1[:, 0]) - r1)
+    ratio = err(1 / 32) / err(1 / 64)
+    assert 7.0 <= ratio <= 9.0, ratio
+
+
+def test_leapfrog_free_particle_and_energy():
+    m = np.array([1.0, 1e-300])
+    x = np.array([[0.0, 5.0], [0.0, 0.0], [0.0, 0.0]])
+    v = np.array([[0.3, 0.0], [-0.2, 0.0], [0.1, 0.0]])
+    x1, v1, _ = oracle.leapfrog(m, x, v, 0.0, 1.0 / 64, 64)
+    assert np.max(np.abs(x1[:, 0] - (x[:, 0] + v[:, 0]))) < 1e-14
+    _, (m, x, v, x1, v1) = _kepler_lf_err(0.5, 6434)
+    E0 = sum(oracle.energy(m, x, v, 0.0))
+    E1 = sum(oracle.energy(m, x1, v1, 0.0))
+    assert abs((E1 - E0) / E0) < 1e-5      # symplectic: bounded, O(dt^2) energy error
