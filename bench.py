@@ -29,7 +29,8 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-FLOPS_PER_INTERACTION = 40   # executed FP32 flops, FFMA = 2 (ncu-checked)
+# executed FP32 flops per interaction, FFMA = 2 (R#20; ncu-checked)
+FLOPS = {"hermite": 40, "leapfrog": 18}
 FP32_LANES_PER_SM = 128      # FP32 FMA lanes per SM (4 SMSP x 32)
 
 
@@ -39,6 +40,7 @@ def parse():
     p.add_argument("--steps", type=int, default=10)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--config", default="C4")
+    p.add_argument("--integrator", default="hermite", choices=["hermite", "leapfrog"])
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -219,7 +221,8 @@ def main():
         nccl_id = obj[0]
 
     sim = binding.NBody(mt, xt, vt, eps=c.eps, dt=c.dt, rank=rank, world=world,
-                        nccl_id=nccl_id, device=local)
+                        nccl_id=nccl_id, device=local, integrator=args.integrator)
+    FLOPS_PER_INTERACTION = FLOPS[args.integrator]
     stream = torch.cuda.current_stream(dev)
     flush = None if args.no_flush else torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
@@ -272,7 +275,8 @@ def main():
     try:
         with open(os.path.join(ROOT, "profiles", "force_traffic.json")) as f:
             tr = json.load(f)
-            if tr.get("config") == args.config and tr.get("n_gpus", 1) == world:
+            if (tr.get("config") == args.config and tr.get("n_gpus", 1) == world
+                    and tr.get("integrator", "hermite") == args.integrator):
                 traffic = tr.get("dram_bytes_per_launch")
     except Exception:
         pass
@@ -324,8 +328,11 @@ def main():
             "dtype": "f32",
             "data": "synthetic",
             "config": {
-                "workload": f"{args.config}: {c.kind} N={n} eps={c.eps} dt=1/1024, "
-                            f"Hermite-4 P(EC)^1 step (predict, all-gather, force, correct)",
+                "workload": f"{args.config}: {c.kind} N={n} eps={c.eps} dt=1/1024, " + (
+                    "Hermite-4 P(EC)^1 step (predict, all-gather, acc+jerk force, correct)"
+                    if args.integrator == "hermite" else
+                    "kick-drift-kick leapfrog step (kick+drift, all-gather, acc force, kick)"),
+                "integrator": args.integrator,
                 "n": n, "flops_per_interaction": FLOPS_PER_INTERACTION,
                 "l2": "flushed between steps (256 MiB memset outside the per-step events)"
                       if flush is not None else "not flushed",

@@ -132,7 +132,8 @@ int nbody_local_range(const nbody_ctx* ctx, int64_t* i0, int64_t* i1);
 /* Evaluates acceleration and jerk of every local particle at the current
  * state (jerk R#2), caches them as the Hermite a0, j0 and writes
  * them, stream-ordered, to acc / jerk ([3][i1 - i0] each; either may be
- * NULL).  G m_j (r_j - r_i) / (r^2 + eps^2)^{3/2} summed over all j in FP32
+ * NULL).  With NBODY_LEAPFROG_KDK only the acceleration is evaluated (the
+ * 18-flop acceleration-only kernel) and a non-NULL jerk is zero-filled.  G m_j (r_j - r_i) / (r^2 + eps^2)^{3/2} summed over all j in FP32
  * per 256-j tile, tiles and chunks folded in fp64 in a fixed order.
  * With eps > 0 the j == i term is exactly zero.  Collective. */
 int nbody_compute_forces(nbody_ctx* ctx, double* acc, double* jerk);
@@ -140,7 +141,9 @@ int nbody_compute_forces(nbody_ctx* ctx, double* acc, double* jerk);
 /* Advances the state by nsteps >= 1 shared-dt steps of the configured
  * integrator.  Hermite: evaluates a0, j0 first if not cached, then per step
  * predict (fp64) -> exchange -> force (FP32) -> correct (fp64): exactly one
- * force evaluation per step (P(EC)^1, R#3).  Non-blocking; a non-finite
+ * force evaluation per step (P(EC)^1, R#3).  Leapfrog (NEXT f1): kick
+ * v += a dt/2, drift x += v dt -> exchange -> acceleration-only force pass ->
+ * kick v += a dt/2, one evaluation per step.  Non-blocking; a non-finite
  * state is reported by the next blocking call.  Collective. */
 int nbody_step(nbody_ctx* ctx, int32_t nsteps);
 

@@ -124,8 +124,9 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t
         : "memory");
 }
 
-template <bool kGuard>
+template <bool kGuard, bool kJerk>
 __global__ void __launch_bounds__(kThreads, FK_MINB) force_kernel(ForceArgs a) {
+    constexpr int kNC = kJerk ? 6 : 3;   // accumulated components: a (+ jerk)
     extern __shared__ __align__(128) unsigned char smem[];
     JPkt* ring = reinterpret_cast<JPkt*>(smem);
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kTileBytes);
@@ -167,11 +168,11 @@ __global__ void __launch_bounds__(kThreads, FK_MINB) force_kernel(ForceArgs a) {
     double* acc_s = reinterpret_cast<double*>(smem + kStages * kTileBytes + 64);
 #define ACC64(k, l) acc_s[((k) * 2 * kPairs + (l)) * kThreads + tid]
 #else
-    double acc64[6][2 * kPairs];
+    double acc64[kNC][2 * kPairs];
 #define ACC64(k, l) acc64[k][l]
 #endif
 #pragma unroll
-    for (int k = 0; k < 6; ++k)
+    for (int k = 0; k < kNC; ++k)
 #pragma unroll
         for (int l = 0; l < 2 * kPairs; ++l) ACC64(k, l) = 0.0;
 
@@ -195,27 +196,32 @@ __global__ void __launch_bounds__(kThreads, FK_MINB) force_kernel(ForceArgs a) {
         mbar_wait(&full[s], (uint32_t)((t / kStages) & 1));
         const JPkt* tile = ring + s * kTile;
 
-        f2 ax[kPairs], ay[kPairs], az[kPairs], jx[kPairs], jy[kPairs], jz[kPairs];
+        f2 acc[kNC][kPairs];
 #pragma unroll
-        for (int p = 0; p < kPairs; ++p) ax[p] = ay[p] = az[p] = jx[p] = jy[p] = jz[p] = 0ull;
+        for (int k = 0; k < kNC; ++k)
+#pragma unroll
+            for (int p = 0; p < kPairs; ++p) acc[k][p] = 0ull;
 
 #pragma unroll kUnroll
         for (int jj = 0; jj < kTile; ++jj) {
-            const int jl = jj;
 #if NB_PKT_DUP
             // j operands arrive as {v, v} register pairs (packet layout, internal.h)
-            const ulonglong2 A = *reinterpret_cast<const ulonglong2*>(&tile[jl].a);
-            const ulonglong2 B = *reinterpret_cast<const ulonglong2*>(&tile[jl].b);
-            const ulonglong2 C = *reinterpret_cast<const ulonglong2*>(&tile[jl].c);
-            const ulonglong2 D = *reinterpret_cast<const ulonglong2*>(&tile[jl].d);
-            const f2 xj = A.x, yj = A.y, zj = B.x, mj = B.y;
-            const f2 vxj = C.x, vyj = C.y, vzj = D.x, eps2 = D.y;
-            const float jmass = tile[jl].b.z;
+            const ulonglong2 A = *reinterpret_cast<const ulonglong2*>(&tile[jj].a);
+            const ulonglong2 B = *reinterpret_cast<const ulonglong2*>(&tile[jj].b);
+            const ulonglong2 D = *reinterpret_cast<const ulonglong2*>(&tile[jj].d);
+            const f2 xj = A.x, yj = A.y, zj = B.x, mj = B.y, eps2 = D.y;
+            f2 vxj = 0, vyj = 0, vzj = 0;
+            if (kJerk) {
+                const ulonglong2 C = *reinterpret_cast<const ulonglong2*>(&tile[jj].c);
+                vxj = C.x; vyj = C.y; vzj = D.x;
+            }
+            const float jmass = tile[jj].b.z;
 #else
-            const float4 P = tile[jl].p;
-            const float4 V = tile[jl].v;
+            const float4 P = tile[jj].p;
+            const float4 V = tile[jj].v;
             const f2 xj = f2bc(P.x), yj = f2bc(P.y), zj = f2bc(P.z), mj = f2bc(P.w);
-            const f2 vxj = f2bc(V.x), vyj = f2bc(V.y), vzj = f2bc(V.z), eps2 = f2bc(V.w);
+            const f2 eps2 = f2bc(V.w);
+            const f2 vxj = f2bc(V.x), vyj = f2bc(V.y), vzj = f2bc(V.z);
             const float jmass = P.w;
 #endif
 #pragma unroll
@@ -223,9 +229,6 @@ __global__ void __launch_bounds__(kThreads, FK_MINB) force_kernel(ForceArgs a) {
                 const f2 dx = fadd2(xj, nx[p]);
                 const f2 dy = fadd2(yj, ny[p]);
                 const f2 dz = fadd2(zj, nz[p]);
-                const f2 wx = fadd2(vxj, nvx[p]);
-                const f2 wy = fadd2(vyj, nvy[p]);
-                const f2 wz = fadd2(vzj, nvz[p]);
                 f2 s2 = ffma2(dx, dx, eps2);
                 s2 = ffma2(dy, dy, s2);
                 s2 = ffma2(dz, dz, s2);
@@ -233,17 +236,16 @@ __global__ void __launch_bounds__(kThreads, FK_MINB) force_kernel(ForceArgs a) {
                 f2split(s2, s_lo, s_hi);
                 float r_lo = rsqrt_ftz(s_lo), r_hi = rsqrt_ftz(s_hi);
                 if (kGuard) {  // eps == 0: exclude j == i (s == 0), R#17
+                    const int64_t jg = jc0 + (int64_t)t * kTile + jj;
                     if (s_lo == 0.f) {
                         r_lo = 0.f;
                         const int64_t ig = a.i_base + ib + (2 * p) * kThreads + tid;
-                        const int64_t jg = jc0 + (int64_t)t * kTile + jj;
                         if (ig != jg && ig < a.i_base + a.n_loc && jmass != 0.f)
                             atomicMin(a.coincident, (unsigned long long)ig);
                     }
                     if (s_hi == 0.f) {
                         r_hi = 0.f;
                         const int64_t ig = a.i_base + ib + (2 * p + 1) * kThreads + tid;
-                        const int64_t jg = jc0 + (int64_t)t * kTile + jj;
                         if (ig != jg && ig < a.i_base + a.n_loc && jmass != 0.f)
                             atomicMin(a.coincident, (unsigned long long)ig);
                     }
@@ -251,29 +253,33 @@ __global__ void __launch_bounds__(kThreads, FK_MINB) force_kernel(ForceArgs a) {
                 const f2 ri = f2make(r_lo, r_hi);
                 const f2 ri2 = fmul2(ri, ri);
                 const f2 mr3 = fmul2(fmul2(mj, ri), ri2);      // G m_j / s^{3/2}
-                f2 rv = fmul2(dx, wx);
-                rv = ffma2(dy, wy, rv);
-                rv = ffma2(dz, wz, rv);                         // d . w
-                const f2 q3 = fmul2(fmul2(rv, ri2), m3);        // -3 (d.w) / s
-                ax[p] = ffma2(mr3, dx, ax[p]);
-                ay[p] = ffma2(mr3, dy, ay[p]);
-                az[p] = ffma2(mr3, dz, az[p]);
-                jx[p] = ffma2(mr3, ffma2(q3, dx, wx), jx[p]);
-                jy[p] = ffma2(mr3, ffma2(q3, dy, wy), jy[p]);
-                jz[p] = ffma2(mr3, ffma2(q3, dz, wz), jz[p]);
+                acc[0][p] = ffma2(mr3, dx, acc[0][p]);
+                acc[1][p] = ffma2(mr3, dy, acc[1][p]);
+                acc[2][p] = ffma2(mr3, dz, acc[2][p]);
+                if (kJerk) {
+                    const f2 wx = fadd2(vxj, nvx[p]);
+                    const f2 wy = fadd2(vyj, nvy[p]);
+                    const f2 wz = fadd2(vzj, nvz[p]);
+                    f2 rv = fmul2(dx, wx);
+                    rv = ffma2(dy, wy, rv);
+                    rv = ffma2(dz, wz, rv);                     // d . w
+                    const f2 q3 = fmul2(fmul2(rv, ri2), m3);    // -3 (d.w) / s
+                    acc[3 % kNC][p] = ffma2(mr3, ffma2(q3, dx, wx), acc[3 % kNC][p]);
+                    acc[4 % kNC][p] = ffma2(mr3, ffma2(q3, dy, wy), acc[4 % kNC][p]);
+                    acc[5 % kNC][p] = ffma2(mr3, ffma2(q3, dz, wz), acc[5 % kNC][p]);
+                }
             }
         }
         // tile sum -> fp64, ascending tile order
 #pragma unroll
-        for (int p = 0; p < kPairs; ++p) {
-            float lo, hi;
-            f2split(ax[p], lo, hi); ACC64(0, 2 * p) += (double)lo; ACC64(0, 2 * p + 1) += (double)hi;
-            f2split(ay[p], lo, hi); ACC64(1, 2 * p) += (double)lo; ACC64(1, 2 * p + 1) += (double)hi;
-            f2split(az[p], lo, hi); ACC64(2, 2 * p) += (double)lo; ACC64(2, 2 * p + 1) += (double)hi;
-            f2split(jx[p], lo, hi); ACC64(3, 2 * p) += (double)lo; ACC64(3, 2 * p + 1) += (double)hi;
-            f2split(jy[p], lo, hi); ACC64(4, 2 * p) += (double)lo; ACC64(4, 2 * p + 1) += (double)hi;
-            f2split(jz[p], lo, hi); ACC64(5, 2 * p) += (double)lo; ACC64(5, 2 * p + 1) += (double)hi;
-        }
+        for (int k = 0; k < kNC; ++k)
+#pragma unroll
+            for (int p = 0; p < kPairs; ++p) {
+                float lo, hi;
+                f2split(acc[k][p], lo, hi);
+                ACC64(k, 2 * p) += (double)lo;
+                ACC64(k, 2 * p + 1) += (double)hi;
+            }
         __syncthreads();  // every warp is done reading stage s
         if (tid == 0 && t + kStages < ntile) {
             mbar_expect_tx(&full[s], kTileBytes);
@@ -282,36 +288,42 @@ __global__ void __launch_bounds__(kThreads, FK_MINB) force_kernel(ForceArgs a) {
         }
     }
 
-    // chunk partial, coalesced fp64 stores
-    double* out = a.partial + (int64_t)c * 6 * a.n_loc_pad;
+    // chunk partial [chunk][kNC][n_loc_pad], coalesced fp64 stores
+    double* out = a.partial + (int64_t)c * kNC * a.n_loc_pad;
 #pragma unroll
     for (int l = 0; l < 2 * kPairs; ++l) {
         const int il = ib + l * kThreads + tid;
         if (il < a.n_loc) {
 #pragma unroll
-            for (int k = 0; k < 6; ++k) out[(int64_t)k * a.n_loc_pad + il] = ACC64(k, l);
+            for (int k = 0; k < kNC; ++k) out[(int64_t)k * a.n_loc_pad + il] = ACC64(k, l);
         }
     }
+#undef ACC64
 }
 
 }  // namespace
 
 int force_i_per_block() { return kIPerBlock; }
 
-cudaError_t launch_force(const ForceArgs& a, bool guard_self, cudaStream_t s) {
-    if (a.c_count <= 0 || a.n_loc <= 0) return cudaSuccess;
-    dim3 grid((unsigned)((a.n_loc + kIPerBlock - 1) / kIPerBlock), (unsigned)a.c_count);
-    static bool attr_set = false;
+template <bool G, bool J>
+cudaError_t launch_one(const ForceArgs& a, dim3 grid, cudaStream_t s) {
+    static bool attr_set = false;   // per instantiation
     if (!attr_set) {
-        cudaFuncSetAttribute(force_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
-        cudaFuncSetAttribute(force_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+        cudaError_t e = cudaFuncSetAttribute(force_kernel<G, J>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+        if (e != cudaSuccess) return e;
         attr_set = true;
     }
-    if (guard_self)
-        force_kernel<true><<<grid, kThreads, kSmemBytes, s>>>(a);
-    else
-        force_kernel<false><<<grid, kThreads, kSmemBytes, s>>>(a);
+    force_kernel<G, J><<<grid, kThreads, kSmemBytes, s>>>(a);
     return cudaGetLastError();
+}
+
+cudaError_t launch_force(const ForceArgs& a, bool guard_self, bool jerk, cudaStream_t s) {
+    if (a.c_count <= 0 || a.n_loc <= 0) return cudaSuccess;
+    dim3 grid((unsigned)((a.n_loc + kIPerBlock - 1) / kIPerBlock), (unsigned)a.c_count);
+    if (jerk)
+        return guard_self ? launch_one<true, true>(a, grid, s) : launch_one<false, true>(a, grid, s);
+    return guard_self ? launch_one<true, false>(a, grid, s) : launch_one<false, false>(a, grid, s);
 }
 
 }  // namespace nb

@@ -7,6 +7,8 @@
 //   correct_predict_pack  fold chunk partials -> a1, j1; Hermite corrector;
 //                         a0 <- a1, j0 <- j1; predictor for the next step;
 //                         packets -> the exchange buffer
+// With integrator == NBODY_LEAPFROG_KDK (NEXT f1) the same two kernels do the
+// kick-drift and the closing kick of kick-drift-kick on accelerations only.
 // Integrator reading R#3: 4th-order Hermite P(EC)^1 with shared dt and the
 // Makino-Aarseth a2/a3 corrector:
 //   xp = x + v dt + a0 dt^2/2 + j0 dt^3/6,  vp = v + a0 dt + j0 dt^2/2
@@ -50,6 +52,8 @@ __global__ void pack_state_kernel(StateArgs a) {
     }
 }
 
+// Hermite (R#3): Taylor predictor.  Leapfrog (NEXT f1): the kick + drift half
+// of kick-drift-kick, vp = v + a dt/2 (the half-step velocity), xp = x + vp dt.
 __device__ __forceinline__ void predict(const StateArgs& a, int i, const double x[3],
                                         const double v[3], const double ac[3],
                                         const double jk[3]) {
@@ -57,8 +61,13 @@ __device__ __forceinline__ void predict(const StateArgs& a, int i, const double 
     double xp[3], vp[3];
     bool ok = true;
     for (int c = 0; c < 3; ++c) {
-        xp[c] = x[c] + v[c] * dt + ac[c] * dt2 / 2.0 + jk[c] * dt3 / 6.0;
-        vp[c] = v[c] + ac[c] * dt + jk[c] * dt2 / 2.0;
+        if (a.integrator == 0) {
+            xp[c] = x[c] + v[c] * dt + ac[c] * dt2 / 2.0 + jk[c] * dt3 / 6.0;
+            vp[c] = v[c] + ac[c] * dt + jk[c] * dt2 / 2.0;
+        } else {
+            vp[c] = v[c] + ac[c] * dt / 2.0;
+            xp[c] = x[c] + vp[c] * dt;
+        }
         a.xp[c * a.n_loc_pad + i] = xp[c];
         a.vp[c * a.n_loc_pad + i] = vp[c];
         ok = ok && isfinite(xp[c]) && isfinite(vp[c]);
@@ -82,9 +91,10 @@ __global__ void predict_pack_kernel(StateArgs a) {
 
 // canonical fold: ascending chunk order, fp64 left fold from +0
 __device__ __forceinline__ double fold(const StateArgs& a, int k, int i) {
+    if (k >= a.ncomp) return 0.0;   // leapfrog: no jerk
     double s = 0.0;
     const double* p = a.partial + (int64_t)k * a.n_loc_pad + i;
-    const int64_t stride = 6 * a.n_loc_pad;
+    const int64_t stride = (int64_t)a.ncomp * a.n_loc_pad;
     for (int c = 0; c < a.n_chunks; ++c) s += p[c * stride];
     return s;
 }
@@ -111,11 +121,16 @@ __global__ void correct_predict_pack_kernel(StateArgs a) {
             const int64_t o = c * a.n_loc_pad + i;
             a1[c] = fold(a, c, i);
             j1[c] = fold(a, 3 + c, i);
-            const double a0 = a.a0[o], j0 = a.j0[o];
-            const double a2 = (-6.0 * (a0 - a1[c]) - dt * (4.0 * j0 + 2.0 * j1[c])) / dt2;
-            const double a3 = (12.0 * (a0 - a1[c]) + 6.0 * dt * (j0 + j1[c])) / dt3;
-            x[c] = a.xp[o] + a2 * dt4 / 24.0 + a3 * dt5 / 120.0;
-            v[c] = a.vp[o] + a2 * dt3 / 6.0 + a3 * dt4 / 24.0;
+            if (a.integrator == 0) {   // Hermite corrector (R#3)
+                const double a0 = a.a0[o], j0 = a.j0[o];
+                const double a2 = (-6.0 * (a0 - a1[c]) - dt * (4.0 * j0 + 2.0 * j1[c])) / dt2;
+                const double a3 = (12.0 * (a0 - a1[c]) + 6.0 * dt * (j0 + j1[c])) / dt3;
+                x[c] = a.xp[o] + a2 * dt4 / 24.0 + a3 * dt5 / 120.0;
+                v[c] = a.vp[o] + a2 * dt3 / 6.0 + a3 * dt4 / 24.0;
+            } else {                   // leapfrog: closing kick
+                x[c] = a.xp[o];
+                v[c] = a.vp[o] + a1[c] * dt / 2.0;
+            }
             a.x[o] = x[c];
             a.v[o] = v[c];
             a.a0[o] = a1[c];

@@ -63,13 +63,14 @@ struct ForceArgs {
     int32_t c_first;     // first chunk of this launch
     int32_t c_count;     // chunks in this launch (grid.y)
     float eps2;          // fp32(eps^2)
-    double* partial;     // [n_chunks][6][n_loc_pad] (acc x,y,z, jerk x,y,z)
+    double* partial;     // [n_chunks][ncomp][n_loc_pad] (acc x,y,z [, jerk x,y,z])
     unsigned long long* coincident;  // eps == 0 only: min global i of a coincident pair
 };
 
 // Launches the force pass for chunks c_first .. c_first + c_count - 1 (mod
-// n_chunks) over all local i.  Returns the launch error.
-cudaError_t launch_force(const ForceArgs& a, bool guard_self, cudaStream_t s);
+// n_chunks) over all local i; jerk == false is the acceleration-only kernel
+// (leapfrog, NEXT f1; partial has 3 components).  Returns the launch error.
+cudaError_t launch_force(const ForceArgs& a, bool guard_self, bool jerk, cudaStream_t s);
 int force_i_per_block();
 
 // fp64 particle-update kernels (hermite.cu).
@@ -81,8 +82,10 @@ struct StateArgs {
     float eps2;          // fp32(eps^2), written into the packets' spare lanes
     const double* m;     // [n_loc]
     double *x, *v, *a0, *j0, *xp, *vp;  // [3][n_loc_pad]
-    const double* partial;  // [n_chunks][6][n_loc_pad]
+    const double* partial;  // [n_chunks][ncomp][n_loc_pad]
     int32_t n_chunks;
+    int32_t ncomp;       // 6 (Hermite: acc + jerk) or 3 (leapfrog: acc)
+    int32_t integrator;  // NBODY_HERMITE4 (0) or NBODY_LEAPFROG_KDK (1)
     JPkt* pkt;           // all packets; local particle i goes to pkt[i_base + i]
     unsigned long long* bad;  // min global index of a non-finite particle
 };

@@ -184,6 +184,8 @@ int fail(nbody_ctx* c, int code, const char* fmt, ...) {
         CK(ctx, cudaSetDevice((ctx)->cfg.device));                                          \
     } while (0)
 
+int ncomp(const nbody_ctx* c) { return c->cfg.integrator == NBODY_HERMITE4 ? 6 : 3; }
+
 nb::StateArgs state_args(nbody_ctx* c, Shard& s) {
     nb::StateArgs a;
     a.n_loc = s.n_loc;
@@ -196,6 +198,8 @@ nb::StateArgs state_args(nbody_ctx* c, Shard& s) {
     a.x = s.x; a.v = s.v; a.a0 = s.a0; a.j0 = s.j0; a.xp = s.xp; a.vp = s.vp;
     a.partial = s.partial;
     a.n_chunks = (int32_t)s.plan.n_chunks;
+    a.ncomp = ncomp(c);
+    a.integrator = c->cfg.integrator;
     a.pkt = c->pkt;
     a.bad = c->flags;
     return a;
@@ -231,7 +235,7 @@ int launch_force_range(nbody_ctx* c, Shard& s, int32_t c_first, int32_t c_count)
         c->prof_used += 2;
         CK(c, cudaEventRecord(e0, c->stream));
     }
-    CK(c, nb::launch_force(f, c->eps2f == 0.f, c->stream));
+    CK(c, nb::launch_force(f, c->eps2f == 0.f, c->cfg.integrator == NBODY_HERMITE4, c->stream));
     if (e1) CK(c, cudaEventRecord(e1, c->stream));
     c->n_force++;
     c->n_kernels++;
@@ -359,7 +363,7 @@ int init_impl(const nbody_config* cfg, const double* m, const double* x, const d
     if (!(std::isfinite(k.G) && k.G > 0)) return fail(c, NBODY_EINVAL, "G must be finite and > 0");
     if (!(std::isfinite(k.eps) && k.eps >= 0)) return fail(c, NBODY_EINVAL, "eps must be finite and >= 0");
     if (!(std::isfinite(k.dt) && k.dt > 0)) return fail(c, NBODY_EINVAL, "dt must be finite and > 0");
-    if (k.integrator != NBODY_HERMITE4)
+    if (k.integrator != NBODY_HERMITE4 && k.integrator != NBODY_LEAPFROG_KDK)
         return fail(c, NBODY_EINVAL, "integrator %d not supported", k.integrator);
     if (!m || !x || !v) return fail(c, NBODY_EINVAL, "m, x and v must be non-NULL");
     if (k.world > 1 && !k.loopback && !k.nccl_id)
@@ -404,7 +408,7 @@ int init_impl(const nbody_config* cfg, const double* m, const double* x, const d
         if ((rc = dalloc(c, &s.x, v3)) || (rc = dalloc(c, &s.v, v3)) || (rc = dalloc(c, &s.a0, v3)) ||
             (rc = dalloc(c, &s.j0, v3)) || (rc = dalloc(c, &s.xp, v3)) || (rc = dalloc(c, &s.vp, v3)))
             return rc;
-        if ((rc = dalloc(c, &s.partial, (size_t)s.plan.n_chunks * 6 * s.n_loc_pad))) return rc;
+        if ((rc = dalloc(c, &s.partial, (size_t)s.plan.n_chunks * ncomp(c) * s.n_loc_pad))) return rc;
         // local chunks: those inside [i0, i0 + slot) of this rank's exchange slice
         const int64_t lo = s.plan.i0 == s.plan.i1 ? 0 : s.plan.i0;
         const int64_t hi = s.plan.i0 == s.plan.i1 ? 0 : s.plan.i0 + s.plan.slot;

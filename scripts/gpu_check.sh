@@ -6,3 +6,4 @@ timeout 1200 python -m pytest tests -m gpu -q --timeout 900 -p no:cacheprovider 
 tail -30 gpurun_out/pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?"; tail -5 gpurun_out/smoke.log
 timeout 600 python bench.py > gpurun_out/bench.log 2>&1; echo "bench rc=$?"; tail -5 gpurun_out/bench.log
+timeout 600 python bench.py --integrator leapfrog --no-cpu-baseline > gpurun_out/bench_lf.log 2>&1; echo "bench lf rc=$?"; tail -2 gpurun_out/bench_lf.log
