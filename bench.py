@@ -114,6 +114,46 @@ class ClockSampler:
                 "samples": len(sm), "reasons": sorted(reasons)}
 
 
+class EnergyMeter:
+    """GPU energy over a region from NVML's total-energy counter (mJ), the B200 form
+    of the paper's energy-to-solution measurement (NEXT f3); host-package
+    energy from RAPL sysfs when the box exposes it."""
+
+    def __init__(self, index):
+        self.h = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+        except Exception:
+            self.h = None
+        self.rapl = [os.path.join(r, "energy_uj") for r in
+                     sorted(__import__("glob").glob("/sys/class/powercap/intel-rapl:[0-9]*"))
+                     if os.path.exists(os.path.join(r, "energy_uj"))]
+
+    def _read(self):
+        g = self.nv.nvmlDeviceGetTotalEnergyConsumption(self.h) / 1e3 if self.h else None
+        c = None
+        try:
+            c = sum(int(open(f).read()) for f in self.rapl) / 1e6 if self.rapl else None
+        except Exception:
+            c = None
+        return g, c
+
+    def start(self):
+        self.t0 = time.perf_counter()
+        self.e0 = self._read()
+
+    def stop(self):
+        t = time.perf_counter() - self.t0
+        e1 = self._read()
+        g = (e1[0] - self.e0[0]) if e1[0] is not None and self.e0[0] is not None else None
+        c = (e1[1] - self.e0[1]) if e1[1] is not None and self.e0[1] is not None else None
+        return {"gpu_joules": g, "host_cpu_joules": c, "seconds": t,
+                "gpu_avg_w": g / t if g is not None and t > 0 else None}
+
+
 def cpu_baseline(m, x, v, eps2, budget_s):
     """The fp64 oracle as it stands, timed on the host cores on a bounded
     sample of the same workload: forces on n_s strided i against all N j."""
@@ -238,10 +278,12 @@ def main():
     sim.prof_read(reset=True)
 
     clocks = ClockSampler(local)
+    meter = EnergyMeter(local)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
     barrier()
     clocks.start()
+    meter.start()
     for k in range(args.steps):
         if flush is not None:
             flush.zero_()                     # L2 flush between steps, outside the step events
@@ -249,6 +291,7 @@ def main():
         sim.step(1)
         ev[k][1].record(stream)
     barrier()
+    energy = meter.stop()
     clk = clocks.stop()
     sim.sync()
     ms_steps = sum(a.elapsed_time(b) for a, b in ev)
@@ -350,6 +393,11 @@ def main():
                               f"({'MEASURED_PEAKS.json sm_max_mhz' if peaks.get('sm_max_mhz') else 'nvidia-smi max clock'})",
             },
             "clocks": clk,
+            "energy": dict(energy, joules_per_step=(energy["gpu_joules"] / args.steps
+                                                    if energy["gpu_joules"] is not None else None),
+                           interactions_per_joule=(float(n) * n * args.steps / energy["gpu_joules"]
+                                                   if energy["gpu_joules"] else None),
+                           scope="this rank's GPU (NVML total-energy counter) over the timed region"),
             "gpu_launches": launches,
             "e2e": e2e,
             "cpu_baseline": cpu,

@@ -137,6 +137,9 @@ struct nbody_ctx {
     cudaEvent_t ev_packed = nullptr, ev_gathered = nullptr;
     ncclComm_t comm = nullptr;
     bool have_a0 = false, predicted = false;
+    bool use_graph = true;
+    cudaGraphExec_t step_graph = nullptr;
+    int64_t graph_kernels = 0, graph_force = 0;
     bool prof = false;
     std::vector<cudaEvent_t> prof_ev;  // pairs
     size_t prof_used = 0;
@@ -326,6 +329,7 @@ void free_ctx(nbody_ctx* c) {
     if (!c) return;
     cudaSetDevice(c->cfg.device);
     if (c->stream) cudaStreamSynchronize(c->stream);
+    if (c->step_graph) cudaGraphExecDestroy(c->step_graph);
     if (c->comm && nccl().ok) nccl().CommDestroy(c->comm);
     for (auto& s : c->sh) {
         cudaFree(s.m); cudaFree(s.x); cudaFree(s.v); cudaFree(s.a0); cudaFree(s.j0);
@@ -370,6 +374,8 @@ int init_impl(const nbody_config* cfg, const double* m, const double* x, const d
         return fail(c, NBODY_EINVAL, "world > 1 needs nccl_id (or loopback)");
     c->cfg = k;
     c->n = k.n;
+    const char* ng = getenv("NBODY_NO_GRAPH");
+    c->use_graph = !(ng && *ng && *ng != '0');
     c->eps2f = (float)(k.eps * k.eps);
     c->nshards = k.loopback ? k.world : 1;
     c->sh.resize(c->nshards);
@@ -518,6 +524,19 @@ int nbody_compute_forces(nbody_ctx* c, double* acc, double* jerk) {
     return NBODY_OK;
 }
 
+namespace {
+// one steady-state step: exchange + force (+ overlap) then fold/correct/predict/pack
+int one_step(nbody_ctx* c) {
+    int rc;
+    if ((rc = exchange_and_force(c))) return rc;
+    for (auto& s : c->sh) {
+        CK(c, nb::launch_correct_predict_pack(state_args(c, s), c->stream));
+        c->n_kernels++;
+    }
+    return NBODY_OK;
+}
+}  // namespace
+
 int nbody_step(nbody_ctx* c, int32_t nsteps) {
     GUARD(c);
     if (nsteps < 1) return fail(c, NBODY_EINVAL, "nsteps must be >= 1");
@@ -530,11 +549,33 @@ int nbody_step(nbody_ctx* c, int32_t nsteps) {
         }
         c->predicted = true;
     }
+    // Steady-state steps replay one captured CUDA graph (fork/join over the comm
+    // stream included) unless kernel timing is on or the stream cannot capture.
+    const bool graph_ok = !c->prof && c->use_graph && c->stream != cudaStreamLegacy &&
+                          c->stream != cudaStreamPerThread && c->stream != nullptr;
+    if (graph_ok && !c->step_graph) {
+        const int64_t nk0 = c->n_kernels, nf0 = c->n_force;
+        CK(c, cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+        rc = one_step(c);
+        cudaGraph_t g = nullptr;
+        cudaError_t e = cudaStreamEndCapture(c->stream, &g);
+        if (rc) { if (g) cudaGraphDestroy(g); return rc; }
+        CK(c, e);
+        e = cudaGraphInstantiate(&c->step_graph, g, 0);
+        cudaGraphDestroy(g);
+        CK(c, e);
+        c->graph_kernels = c->n_kernels - nk0;
+        c->graph_force = c->n_force - nf0;
+        c->n_kernels = nk0;
+        c->n_force = nf0;
+    }
     for (int32_t t = 0; t < nsteps; ++t) {
-        if ((rc = exchange_and_force(c))) return rc;
-        for (auto& s : c->sh) {
-            CK(c, nb::launch_correct_predict_pack(state_args(c, s), c->stream));
-            c->n_kernels++;
+        if (graph_ok) {
+            CK(c, cudaGraphLaunch(c->step_graph, c->stream));
+            c->n_kernels += c->graph_kernels;
+            c->n_force += c->graph_force;
+        } else if ((rc = one_step(c))) {
+            return rc;
         }
     }
     return NBODY_OK;

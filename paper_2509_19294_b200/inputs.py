@@ -49,6 +49,10 @@ CONFIGS = {
     "C3": Config("C3", 131072, "plummer", 1e-3, 1.0 / 1024, 20, 3, (1, 2, 4, 8)),
     "C4": Config("C4", 262144, "two_cluster", 1e-3, 1.0 / 1024, 10, 4, (1, 2, 4, 8)),
     "C5": Config("C5", 1048576, "plummer", 5e-4, 1.0 / 1024, 5, 5, (1, 2, 4, 8)),
+    # NEXT f4: the paper's own workload shape, 102400 particles over "ten time
+    # cycles"; ICs, softening and dt unstated -> Plummer, eps 1e-3,
+    # dt 1/1024, one cycle = one Hermite step (R#4, R#24).
+    "PAPER": Config("PAPER", 102400, "plummer", 1e-3, 1.0 / 1024, 10, 6, (1,)),
 }
 
 

@@ -1,0 +1,78 @@
+#!/usr/bin/env python
+"""NEXT f4 (+ f3): the paper-shaped run on one B200 -- Plummer N = 102 400, ten Hermite
+steps ("ten time cycles") -- with time-to-solution bracketed like the paper's
+MPI_Wtime and energy-to-solution from NVML's GPU energy counter over the
+simulation window with idle padding before/after (5 s instead of
+120 s).  Prints one JSON line; the paper's numbers are quoted as context only
+(other hardware, unknown ICs).
+
+  python scripts/paper_run.py [--repeats 5] [--pad 5]
+"""
+import argparse
+import json
+import os
+import statistics
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--repeats", type=int, default=5)
+    ap.add_argument("--pad", type=float, default=5.0)
+    ap.add_argument("--integrator", default="hermite")
+    a = ap.parse_args()
+    import numpy as np
+    import torch
+    from bench import EnergyMeter
+    from paper_2509_19294_b200 import binding, inputs
+    c = inputs.CONFIGS["PAPER"]
+    m, x, v = inputs.make("PAPER")
+    hm, hx, hv = (torch.from_numpy(t).pin_memory() for t in (m, x, v))
+    torch.cuda.set_device(0)
+    # warm-up: module load, first-touch allocations
+    with binding.NBody(hm, hx, hv, eps=c.eps, dt=c.dt, integrator=a.integrator) as s:
+        s.step(1)
+        s.sync()
+    meter = EnergyMeter(0)
+    runs = []
+    for r in range(a.repeats):
+        time.sleep(a.pad)
+        meter.start()
+        t0 = time.perf_counter()
+        with binding.NBody(hm, hx, hv, eps=c.eps, dt=c.dt, integrator=a.integrator) as s:
+            s.step(c.steps)                    # includes the t = 0 force evaluation
+            xo = np.empty((3, c.n))
+            vo = np.empty((3, c.n))
+            binding._check(binding.lib().nbody_get_state(s._ctx, xo.ctypes.data, vo.ctypes.data), s._ctx)
+            ke, pe = s.energy()
+        t = time.perf_counter() - t0
+        e = meter.stop()
+        runs.append({"seconds": t, "gpu_joules": e["gpu_joules"], "energy_after": ke + pe})
+        time.sleep(a.pad)
+    ts = [r["seconds"] for r in runs]
+    es = [r["gpu_joules"] for r in runs if r["gpu_joules"] is not None]
+    out = {
+        "workload": f"PAPER: Plummer N={c.n} eps={c.eps} dt=1/1024, {c.steps} {a.integrator} steps "
+                    "(+ t=0 force evaluation, final state D2H and fp64 energy)",
+        "time_to_solution_s": {"mean": statistics.mean(ts), "stdev": statistics.pstdev(ts),
+                               "min": min(ts), "max": max(ts), "runs": len(ts)},
+        "energy_to_solution_j": ({"mean": statistics.mean(es), "stdev": statistics.pstdev(es),
+                                  "runs": len(es), "scope": "1 GPU, NVML total-energy counter"}
+                                 if es else None),
+        "paper_context_other_hardware": {
+            "wormhole_n300_plus_1_host_thread_s": "301.40 +- 0.24 (P:191)",
+            "cpu_2x_epyc9124_32_threads_s": "672.90 +- 7.83 (P:191)",
+            "energy_kJ": "71.56 +- 0.13 (Wormhole) vs 128.89 +- 1.52 (CPU) (P:236-237)",
+            "note": "paper ICs, softening, dt and 'time cycle' unstated; not comparable targets",
+        },
+        "runs": runs,
+    }
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()

@@ -303,3 +303,21 @@ def test_coincident_pair_eps0_is_reported_and_sticky():
         s.step(1)
     assert e2.value.code == binding.NBODY_ESTATE
     s.close()
+
+
+def test_cuda_graph_replay_bit_identical(monkeypatch):
+    """Steady-state steps replay a captured CUDA graph on a non-default stream; the
+    result equals eager launches (NBODY_NO_GRAPH=1) bit for bit."""
+    m, x, v = inputs.make("C1")
+    out = []
+    for no_graph in ("0", "1"):
+        monkeypatch.setenv("NBODY_NO_GRAPH", no_graph)
+        st = torch.cuda.Stream()
+        with binding.NBody(m, x, v, eps=1e-2, dt=1 / 1024, stream=st) as s:
+            s.step(5)
+            s.step(5)
+            xs, vs = s.state()
+            s.sync()
+            st.synchronize()
+            out.append((xs.cpu().numpy(), vs.cpu().numpy()))
+    assert np.array_equal(out[0][0], out[1][0]) and np.array_equal(out[0][1], out[1][1])
