@@ -86,6 +86,11 @@ typedef struct {
                              NCCL).  Outputs then cover all n particles.       */
     int32_t jchunks;      /* max number of j-chunks of the canonical reduction
                              (0 -> 128).  Must be equal on every rank.          */
+    int32_t hilo;         /* != 0: two-float positions (NEXT f2): packets also
+                             carry lo = fp32(x - fp32(x)) and the force kernel
+                             forms d = (xj_hi - xi_hi) + (xj_lo - xi_lo), so
+                             fp64 states off the fp32 grid keep ~1e-6 relative
+                             force error (+6 FADD per interaction).            */
     const uint8_t* nccl_id; /* 128-byte ncclUniqueId from nbody_nccl_unique_id
                              on rank 0, broadcast by the caller; required when
                              world > 1 and loopback == 0; optional with

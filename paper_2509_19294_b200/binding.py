@@ -43,6 +43,7 @@ class Config(ctypes.Structure):
         ("world", ctypes.c_int32),
         ("loopback", ctypes.c_int32),
         ("jchunks", ctypes.c_int32),
+        ("hilo", ctypes.c_int32),
         ("nccl_id", ctypes.c_void_p),
         ("stream", ctypes.c_void_p),
     ]
@@ -144,7 +145,7 @@ class NBody:
     """
 
     def __init__(self, m, x, v, eps, dt, G=1.0, integrator="hermite", rank=0, world=1,
-                 loopback=False, nccl_id=None, device=None, stream=None, jchunks=0):
+                 loopback=False, nccl_id=None, device=None, stream=None, jchunks=0, hilo=False):
         import torch
         if not torch.cuda.is_available():
             raise NBodyError(NBODY_ECUDA, "no CUDA device: libnbody has no CPU path")
@@ -162,7 +163,7 @@ class NBody:
         cfg = Config(n=n, G=float(G), eps=float(eps), dt=float(dt),
                      integrator={"hermite": NBODY_HERMITE4, "leapfrog": NBODY_LEAPFROG_KDK}[integrator],
                      device=int(device), rank=int(rank), world=int(world),
-                     loopback=1 if loopback else 0, jchunks=int(jchunks),
+                     loopback=1 if loopback else 0, jchunks=int(jchunks), hilo=1 if hilo else 0,
                      nccl_id=None, stream=raw_stream)
         if nccl_id is not None:
             idbuf = (ctypes.c_uint8 * 128).from_buffer_copy(nccl_id)

@@ -55,8 +55,9 @@ constexpr int kStages = FK_STAGES;        // smem ring depth (tiles)
 constexpr int kUnroll = FK_UNROLL;
 constexpr int kIPerBlock = 2 * kPairs * kThreads;
 constexpr int kTileBytes = kTile * (int)sizeof(JPkt);
+constexpr int kLoTileBytes = kTile * (int)sizeof(float4);   // hi/lo position tails (NEXT f2)
 constexpr int kAccSmemBytes = FK_ACC_SMEM ? 6 * 2 * kPairs * kThreads * 8 : 0;
-constexpr int kSmemBytes = kStages * kTileBytes + 64 + kAccSmemBytes;
+constexpr int kSmemBytes = kStages * (kTileBytes + kLoTileBytes) + 64 + kAccSmemBytes;
 
 typedef unsigned long long f2;  // packed {lo, hi} fp32 pair in one 64-bit register
 
@@ -124,12 +125,14 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t
         : "memory");
 }
 
-template <bool kGuard, bool kJerk>
+template <bool kGuard, bool kJerk, bool kHiLo>
 __global__ void __launch_bounds__(kThreads, FK_MINB) force_kernel(ForceArgs a) {
     constexpr int kNC = kJerk ? 6 : 3;   // accumulated components: a (+ jerk)
+    constexpr uint32_t kStageTx = kTileBytes + (kHiLo ? kLoTileBytes : 0);
     extern __shared__ __align__(128) unsigned char smem[];
     JPkt* ring = reinterpret_cast<JPkt*>(smem);
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kTileBytes);
+    float4* ring_lo = reinterpret_cast<float4*>(smem + kStages * kTileBytes);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * (kTileBytes + kLoTileBytes));
 
     const int tid = threadIdx.x;
     const int c = (a.c_first + (int)blockIdx.y) % a.n_chunks;
@@ -139,9 +142,10 @@ __global__ void __launch_bounds__(kThreads, FK_MINB) force_kernel(ForceArgs a) {
 
     // ---- i-particles: kPairs packed pairs, stored negated (d = x_j + (-x_i))
     f2 nx[kPairs], ny[kPairs], nz[kPairs], nvx[kPairs], nvy[kPairs], nvz[kPairs];
+    f2 nlx[kPairs], nly[kPairs], nlz[kPairs];   // hi/lo: negated low parts
 #pragma unroll
     for (int p = 0; p < kPairs; ++p) {
-        float q[2][6];
+        float q[2][9];
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
             const int il = ib + (2 * p + h) * kThreads + tid;
@@ -150,9 +154,13 @@ __global__ void __launch_bounds__(kThreads, FK_MINB) force_kernel(ForceArgs a) {
                 const float4 P = jpkt_pos(pk), V = jpkt_vel(pk);
                 q[h][0] = -P.x; q[h][1] = -P.y; q[h][2] = -P.z;
                 q[h][3] = -V.x; q[h][4] = -V.y; q[h][5] = -V.z;
+                if (kHiLo) {
+                    const float4 Lo = a.pklo[a.i_base + il];
+                    q[h][6] = -Lo.x; q[h][7] = -Lo.y; q[h][8] = -Lo.z;
+                }
             } else {  // padding i: computed, never stored
-                q[h][0] = q[h][1] = q[h][2] = 0.f;
-                q[h][3] = q[h][4] = q[h][5] = 0.f;
+#pragma unroll
+                for (int k = 0; k < 9; ++k) q[h][k] = 0.f;
             }
         }
         nx[p] = f2make(q[0][0], q[1][0]);
@@ -161,6 +169,13 @@ __global__ void __launch_bounds__(kThreads, FK_MINB) force_kernel(ForceArgs a) {
         nvx[p] = f2make(q[0][3], q[1][3]);
         nvy[p] = f2make(q[0][4], q[1][4]);
         nvz[p] = f2make(q[0][5], q[1][5]);
+        if (kHiLo) {
+            nlx[p] = f2make(q[0][6], q[1][6]);
+            nly[p] = f2make(q[0][7], q[1][7]);
+            nlz[p] = f2make(q[0][8], q[1][8]);
+        } else {
+            nlx[p] = nly[p] = nlz[p] = 0ull;
+        }
     }
 
 #if FK_ACC_SMEM
@@ -184,8 +199,11 @@ __global__ void __launch_bounds__(kThreads, FK_MINB) force_kernel(ForceArgs a) {
     __syncthreads();
     if (tid == 0) {
         for (int s = 0; s < kStages && s < ntile; ++s) {
-            mbar_expect_tx(&full[s], kTileBytes);
+            mbar_expect_tx(&full[s], kStageTx);
             tma_load_1d(ring + s * kTile, a.pkt + jc0 + (int64_t)s * kTile, kTileBytes, &full[s]);
+            if (kHiLo)
+                tma_load_1d(ring_lo + s * kTile, a.pklo + jc0 + (int64_t)s * kTile, kLoTileBytes,
+                            &full[s]);
         }
     }
 
@@ -195,6 +213,7 @@ __global__ void __launch_bounds__(kThreads, FK_MINB) force_kernel(ForceArgs a) {
         const int s = t % kStages;
         mbar_wait(&full[s], (uint32_t)((t / kStages) & 1));
         const JPkt* tile = ring + s * kTile;
+        const float4* tile_lo = ring_lo + s * kTile;
 
         f2 acc[kNC][kPairs];
 #pragma unroll
@@ -224,11 +243,21 @@ __global__ void __launch_bounds__(kThreads, FK_MINB) force_kernel(ForceArgs a) {
             const f2 vxj = f2bc(V.x), vyj = f2bc(V.y), vzj = f2bc(V.z);
             const float jmass = P.w;
 #endif
+            f2 lxj = 0ull, lyj = 0ull, lzj = 0ull;
+            if (kHiLo) {
+                const float4 L = tile_lo[jj];
+                lxj = f2bc(L.x); lyj = f2bc(L.y); lzj = f2bc(L.z);
+            }
 #pragma unroll
             for (int p = 0; p < kPairs; ++p) {
-                const f2 dx = fadd2(xj, nx[p]);
-                const f2 dy = fadd2(yj, ny[p]);
-                const f2 dz = fadd2(zj, nz[p]);
+                f2 dx = fadd2(xj, nx[p]);
+                f2 dy = fadd2(yj, ny[p]);
+                f2 dz = fadd2(zj, nz[p]);
+                if (kHiLo) {   // d = (x_j^hi - x_i^hi) + (x_j^lo - x_i^lo)   (NEXT f2)
+                    dx = fadd2(dx, fadd2(lxj, nlx[p]));
+                    dy = fadd2(dy, fadd2(lyj, nly[p]));
+                    dz = fadd2(dz, fadd2(lzj, nlz[p]));
+                }
                 f2 s2 = ffma2(dx, dx, eps2);
                 s2 = ffma2(dy, dy, s2);
                 s2 = ffma2(dz, dz, s2);
@@ -282,9 +311,12 @@ __global__ void __launch_bounds__(kThreads, FK_MINB) force_kernel(ForceArgs a) {
             }
         __syncthreads();  // every warp is done reading stage s
         if (tid == 0 && t + kStages < ntile) {
-            mbar_expect_tx(&full[s], kTileBytes);
+            mbar_expect_tx(&full[s], kStageTx);
             tma_load_1d(ring + s * kTile, a.pkt + jc0 + (int64_t)(t + kStages) * kTile, kTileBytes,
                         &full[s]);
+            if (kHiLo)
+                tma_load_1d(ring_lo + s * kTile, a.pklo + jc0 + (int64_t)(t + kStages) * kTile,
+                            kLoTileBytes, &full[s]);
         }
     }
 
@@ -305,25 +337,30 @@ __global__ void __launch_bounds__(kThreads, FK_MINB) force_kernel(ForceArgs a) {
 
 int force_i_per_block() { return kIPerBlock; }
 
-template <bool G, bool J>
+template <bool G, bool J, bool H>
 cudaError_t launch_one(const ForceArgs& a, dim3 grid, cudaStream_t s) {
     static bool attr_set = false;   // per instantiation
     if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(force_kernel<G, J>,
+        cudaError_t e = cudaFuncSetAttribute(force_kernel<G, J, H>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
         if (e != cudaSuccess) return e;
         attr_set = true;
     }
-    force_kernel<G, J><<<grid, kThreads, kSmemBytes, s>>>(a);
+    force_kernel<G, J, H><<<grid, kThreads, kSmemBytes, s>>>(a);
     return cudaGetLastError();
+}
+
+template <bool G, bool J>
+cudaError_t launch_gj(const ForceArgs& a, dim3 grid, cudaStream_t s) {
+    return a.pklo ? launch_one<G, J, true>(a, grid, s) : launch_one<G, J, false>(a, grid, s);
 }
 
 cudaError_t launch_force(const ForceArgs& a, bool guard_self, bool jerk, cudaStream_t s) {
     if (a.c_count <= 0 || a.n_loc <= 0) return cudaSuccess;
     dim3 grid((unsigned)((a.n_loc + kIPerBlock - 1) / kIPerBlock), (unsigned)a.c_count);
     if (jerk)
-        return guard_self ? launch_one<true, true>(a, grid, s) : launch_one<false, true>(a, grid, s);
-    return guard_self ? launch_one<true, false>(a, grid, s) : launch_one<false, false>(a, grid, s);
+        return guard_self ? launch_gj<true, true>(a, grid, s) : launch_gj<false, true>(a, grid, s);
+    return guard_self ? launch_gj<true, false>(a, grid, s) : launch_gj<false, false>(a, grid, s);
 }
 
 }  // namespace nb

@@ -32,13 +32,19 @@ __device__ __forceinline__ void flag_bad(unsigned long long* bad, int64_t ig) {
     atomicMin(bad, (unsigned long long)ig);
 }
 
-__device__ __forceinline__ void store_packet(JPkt* dst, const double x[3], const double v[3],
-                                             double gm, float eps2) {
+// fp64 -> fp32 RNE packet (R#18); with hi/lo (NEXT f2) also the fp32 tail
+// lo = RNE(x - hi), so hi + lo carries ~48 bits of the fp64 position.
+__device__ __forceinline__ void store_packet(const StateArgs& a, int64_t k, const double x[3],
+                                             const double v[3], double gm) {
     const float px = __double2float_rn(x[0]), py = __double2float_rn(x[1]);
     const float pz = __double2float_rn(x[2]), pm = __double2float_rn(gm);
     const float qx = __double2float_rn(v[0]), qy = __double2float_rn(v[1]);
     const float qz = __double2float_rn(v[2]);
-    *dst = make_jpkt(px, py, pz, pm, qx, qy, qz, eps2);
+    a.pkt[k] = make_jpkt(px, py, pz, pm, qx, qy, qz, a.eps2);
+    if (a.pklo)
+        a.pklo[k] = make_float4(__double2float_rn(x[0] - (double)px),
+                                __double2float_rn(x[1] - (double)py),
+                                __double2float_rn(x[2] - (double)pz), 0.f);
 }
 
 __global__ void pack_state_kernel(StateArgs a) {
@@ -48,7 +54,7 @@ __global__ void pack_state_kernel(StateArgs a) {
             x[c] = a.x[c * a.n_loc_pad + i];
             v[c] = a.v[c * a.n_loc_pad + i];
         }
-        store_packet(a.pkt + a.i_base + i, x, v, a.G * a.m[i], a.eps2);
+        store_packet(a, a.i_base + i, x, v, a.G * a.m[i]);
     }
 }
 
@@ -73,7 +79,7 @@ __device__ __forceinline__ void predict(const StateArgs& a, int i, const double 
         ok = ok && isfinite(xp[c]) && isfinite(vp[c]);
     }
     if (!ok) flag_bad(a.bad, a.i_base + i);
-    store_packet(a.pkt + a.i_base + i, xp, vp, a.G * a.m[i], a.eps2);
+    store_packet(a, a.i_base + i, xp, vp, a.G * a.m[i]);
 }
 
 __global__ void predict_pack_kernel(StateArgs a) {
@@ -142,11 +148,12 @@ __global__ void correct_predict_pack_kernel(StateArgs a) {
     }
 }
 
-__global__ void fill_padding_kernel(JPkt* pkt, int64_t from, int64_t to, float eps2) {
+__global__ void fill_padding_kernel(JPkt* pkt, float4* pklo, int64_t from, int64_t to, float eps2) {
     for (int64_t k = from + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < to;
          k += (int64_t)gridDim.x * blockDim.x) {
         // zero mass far away: contributes exactly 0 (padding)
         pkt[k] = make_jpkt(1e18f, 1e18f, 1e18f, 0.f, 0.f, 0.f, 0.f, eps2);
+        if (pklo) pklo[k] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
 }
 
@@ -194,9 +201,10 @@ cudaError_t launch_correct_predict_pack(const StateArgs& a, cudaStream_t s) {
     correct_predict_pack_kernel<<<grid_for(a.n_loc), kBlock, 0, s>>>(a);
     return cudaGetLastError();
 }
-cudaError_t launch_fill_padding(JPkt* pkt, int64_t from, int64_t to, float eps2, cudaStream_t s) {
+cudaError_t launch_fill_padding(JPkt* pkt, float4* pklo, int64_t from, int64_t to, float eps2,
+                                cudaStream_t s) {
     if (to <= from) return cudaSuccess;
-    fill_padding_kernel<<<grid_for(to - from), kBlock, 0, s>>>(pkt, from, to, eps2);
+    fill_padding_kernel<<<grid_for(to - from), kBlock, 0, s>>>(pkt, pklo, from, to, eps2);
     return cudaGetLastError();
 }
 

@@ -55,6 +55,7 @@ constexpr int kTile = 256;  // j per fp32 partial-sum tile (R#10)
 // Force pass arguments.  One CTA = (i-block, chunk); see force.cu.
 struct ForceArgs {
     const JPkt* pkt;     // all-gathered j packets [L]
+    const float4* pklo;  // NEXT f2 hi/lo: fp32(x - fp32(x)) tails [L], or nullptr
     int64_t i_base;      // global index of local particle 0
     int32_t n_loc;       // local particles
     int64_t n_loc_pad;   // row stride of `partial`
@@ -87,13 +88,15 @@ struct StateArgs {
     int32_t ncomp;       // 6 (Hermite: acc + jerk) or 3 (leapfrog: acc)
     int32_t integrator;  // NBODY_HERMITE4 (0) or NBODY_LEAPFROG_KDK (1)
     JPkt* pkt;           // all packets; local particle i goes to pkt[i_base + i]
+    float4* pklo;        // hi/lo position tails (nullptr unless hilo)
     unsigned long long* bad;  // min global index of a non-finite particle
 };
 cudaError_t launch_pack_state(const StateArgs& a, cudaStream_t s);     // x, v -> pkt
 cudaError_t launch_predict_pack(const StateArgs& a, cudaStream_t s);   // x,v,a0,j0 -> xp,vp,pkt
 cudaError_t launch_fold_forces(const StateArgs& a, cudaStream_t s);    // partial -> a0, j0
 cudaError_t launch_correct_predict_pack(const StateArgs& a, cudaStream_t s);
-cudaError_t launch_fill_padding(JPkt* pkt, int64_t from, int64_t to, float eps2, cudaStream_t s);
+cudaError_t launch_fill_padding(JPkt* pkt, float4* pklo, int64_t from, int64_t to, float eps2,
+                                cudaStream_t s);
 // bad2[0]: min global index with m not finite or <= 0; bad2[1]: x or v not finite
 cudaError_t launch_validate(const StateArgs& a, unsigned long long* bad2, cudaStream_t s);
 

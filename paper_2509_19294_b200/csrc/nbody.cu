@@ -127,6 +127,7 @@ struct nbody_ctx {
     int nshards = 1;
     std::vector<Shard> sh;
     JPkt* pkt = nullptr;
+    float4* pklo = nullptr;   // hi/lo position tails (cfg.hilo)
     double4* eall = nullptr;
     double* eblk = nullptr;
     int eblk_cap = 0;
@@ -204,6 +205,7 @@ nb::StateArgs state_args(nbody_ctx* c, Shard& s) {
     a.ncomp = ncomp(c);
     a.integrator = c->cfg.integrator;
     a.pkt = c->pkt;
+    a.pklo = c->pklo;
     a.bad = c->flags;
     return a;
 }
@@ -214,6 +216,7 @@ int launch_force_range(nbody_ctx* c, Shard& s, int32_t c_first, int32_t c_count)
     if (c_count <= 0 || s.n_loc <= 0) return NBODY_OK;
     nb::ForceArgs f;
     f.pkt = c->pkt;
+    f.pklo = c->pklo;
     f.i_base = s.plan.i0;
     f.n_loc = s.n_loc;
     f.n_loc_pad = s.n_loc_pad;
@@ -258,6 +261,12 @@ int exchange_and_force(nbody_ctx* c) {
         const size_t cnt = (size_t)s.plan.slot * (sizeof(JPkt) / sizeof(float));
         CKNCCL(c, nccl().AllGather(base + (size_t)c->cfg.rank * cnt, base, cnt, ncclFloat32, c->comm,
                                    c->comm_stream));
+        if (c->pklo) {
+            float* lo = reinterpret_cast<float*>(c->pklo);
+            const size_t cl = (size_t)s.plan.slot * 4;
+            CKNCCL(c, nccl().AllGather(lo + (size_t)c->cfg.rank * cl, lo, cl, ncclFloat32, c->comm,
+                                       c->comm_stream));
+        }
         CK(c, cudaEventRecord(c->ev_gathered, c->comm_stream));
         if ((rc = launch_force_range(c, s, s.c_lo, s.c_hi - s.c_lo))) return rc;
         CK(c, cudaStreamWaitEvent(c->stream, c->ev_gathered, 0));
@@ -336,6 +345,7 @@ void free_ctx(nbody_ctx* c) {
         cudaFree(s.xp); cudaFree(s.vp); cudaFree(s.partial);
     }
     cudaFree(c->pkt);
+    cudaFree(c->pklo);
     cudaFree(c->eall);
     cudaFree(c->eblk);
     cudaFree(c->eout);
@@ -400,9 +410,10 @@ int init_impl(const nbody_config* cfg, const double* m, const double* x, const d
     CK(c, cudaEventCreateWithFlags(&c->ev_gathered, cudaEventDisableTiming));
 
     if ((rc = dalloc(c, &c->pkt, (size_t)c->L))) return rc;
+    if (k.hilo && (rc = dalloc(c, &c->pklo, (size_t)c->L))) return rc;
     if ((rc = dalloc(c, &c->flags, 4))) return rc;
     CK(c, cudaMemsetAsync(c->flags, 0xff, 4 * sizeof(unsigned long long), c->stream));
-    CK(c, nb::launch_fill_padding(c->pkt, 0, c->L, c->eps2f, c->stream));
+    CK(c, nb::launch_fill_padding(c->pkt, c->pklo, 0, c->L, c->eps2f, c->stream));
     c->n_kernels++;
 
     const int64_t ib = nb::force_i_per_block();
