@@ -57,7 +57,12 @@ constexpr int kIPerBlock = 2 * kPairs * kThreads;
 constexpr int kTileBytes = kTile * (int)sizeof(JPkt);
 constexpr int kLoTileBytes = kTile * (int)sizeof(float4);   // hi/lo position tails (NEXT f2)
 constexpr int kAccSmemBytes = FK_ACC_SMEM ? 6 * 2 * kPairs * kThreads * 8 : 0;
-constexpr int kSmemBytes = kStages * (kTileBytes + kLoTileBytes) + 64 + kAccSmemBytes;
+// shared memory layout: [ring: kStages j-tiles][ring_lo: kStages lo-tiles][64 B mbarriers][fp64 acc]
+constexpr int kOffLo = kStages * kTileBytes;
+constexpr int kOffBar = kOffLo + kStages * kLoTileBytes;
+constexpr int kOffAcc = kOffBar + 64;
+constexpr int kSmemBytes = kOffAcc + kAccSmemBytes;
+static_assert(kStages * 8 <= 64, "mbarrier area");
 
 typedef unsigned long long f2;  // packed {lo, hi} fp32 pair in one 64-bit register
 
@@ -131,8 +136,8 @@ __global__ void __launch_bounds__(kThreads, FK_MINB) force_kernel(ForceArgs a) {
     constexpr uint32_t kStageTx = kTileBytes + (kHiLo ? kLoTileBytes : 0);
     extern __shared__ __align__(128) unsigned char smem[];
     JPkt* ring = reinterpret_cast<JPkt*>(smem);
-    float4* ring_lo = reinterpret_cast<float4*>(smem + kStages * kTileBytes);
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * (kTileBytes + kLoTileBytes));
+    float4* ring_lo = reinterpret_cast<float4*>(smem + kOffLo);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kOffBar);
 
     const int tid = threadIdx.x;
     const int c = (a.c_first + (int)blockIdx.y) % a.n_chunks;
@@ -180,7 +185,7 @@ __global__ void __launch_bounds__(kThreads, FK_MINB) force_kernel(ForceArgs a) {
 
 #if FK_ACC_SMEM
     // fp64 chunk accumulators in shared memory: [k][l][tid], conflict-free
-    double* acc_s = reinterpret_cast<double*>(smem + kStages * kTileBytes + 64);
+    double* acc_s = reinterpret_cast<double*>(smem + kOffAcc);
 #define ACC64(k, l) acc_s[((k) * 2 * kPairs + (l)) * kThreads + tid]
 #else
     double acc64[kNC][2 * kPairs];
