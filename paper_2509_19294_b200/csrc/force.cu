@@ -42,6 +42,9 @@ namespace {
 #ifndef FK_MINB
 #define FK_MINB 2
 #endif
+#ifndef FK_MINB_ACC
+#define FK_MINB_ACC 2    // acceleration-only kernel (leapfrog)
+#endif
 #ifndef FK_UNROLL
 #define FK_UNROLL 2
 #endif
@@ -131,7 +134,7 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t
 }
 
 template <bool kGuard, bool kJerk, bool kHiLo>
-__global__ void __launch_bounds__(kThreads, FK_MINB) force_kernel(ForceArgs a) {
+__global__ void __launch_bounds__(kThreads, kJerk ? FK_MINB : FK_MINB_ACC) force_kernel(ForceArgs a) {
     constexpr int kNC = kJerk ? 6 : 3;   // accumulated components: a (+ jerk)
     constexpr uint32_t kStageTx = kTileBytes + (kHiLo ? kLoTileBytes : 0);
     extern __shared__ __align__(128) unsigned char smem[];

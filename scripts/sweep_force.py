@@ -14,20 +14,14 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 OUT = os.path.join(ROOT, "scripts", "sweep")
 
-VARIANTS = {}
-for dup in (0, 1):
-    for name, d in {
-        "base":   dict(FK_THREADS=128, FK_PAIRS=2, FK_MINB=3, FK_UNROLL=4, FK_ACC_SMEM=0),
-        "u2":     dict(FK_THREADS=128, FK_PAIRS=2, FK_MINB=3, FK_UNROLL=2, FK_ACC_SMEM=0),
-        "p4s":    dict(FK_THREADS=128, FK_PAIRS=4, FK_MINB=2, FK_UNROLL=2, FK_ACC_SMEM=1),
-        "p4sU1":  dict(FK_THREADS=128, FK_PAIRS=4, FK_MINB=2, FK_UNROLL=1, FK_ACC_SMEM=1),
-        "p4b2":   dict(FK_THREADS=128, FK_PAIRS=4, FK_MINB=2, FK_UNROLL=2, FK_ACC_SMEM=0),
-        "p3s":    dict(FK_THREADS=128, FK_PAIRS=3, FK_MINB=3, FK_UNROLL=2, FK_ACC_SMEM=1),
-        "p3sb2":  dict(FK_THREADS=128, FK_PAIRS=3, FK_MINB=2, FK_UNROLL=4, FK_ACC_SMEM=1),
-        "p5s":    dict(FK_THREADS=128, FK_PAIRS=5, FK_MINB=2, FK_UNROLL=1, FK_ACC_SMEM=1),
-        "p6sT64": dict(FK_THREADS=64, FK_PAIRS=6, FK_MINB=4, FK_UNROLL=1, FK_ACC_SMEM=1),
-    }.items():
-        VARIANTS[f"d{dup}_{name}"] = dict(d, NB_PKT_DUP=dup)
+VARIANTS = {
+    "lf_b2":    dict(FK_MINB_ACC=2),
+    "lf_b3":    dict(FK_MINB_ACC=3),
+    "lf_b3u4":  dict(FK_MINB_ACC=3, FK_UNROLL=4),
+    "lf_b4p2":  dict(FK_MINB_ACC=4, FK_PAIRS=2, FK_MINB=3),
+    "lf_b3p3":  dict(FK_MINB_ACC=3, FK_PAIRS=3, FK_MINB=2),
+    "lf_b2p5":  dict(FK_MINB_ACC=2, FK_PAIRS=5, FK_MINB=2),
+}
 if os.environ.get("SWEEP_ONLY"):
     VARIANTS = {k: v for k, v in VARIANTS.items() if k in os.environ["SWEEP_ONLY"].split(",")}
 
@@ -60,7 +54,8 @@ def time_one(config, reps):
     m, x, v = inputs.make(config)
     dev = torch.device("cuda", 0)
     sim = binding.NBody(torch.from_numpy(m).to(dev), torch.from_numpy(x).to(dev),
-                        torch.from_numpy(v).to(dev), eps=c.eps, dt=c.dt)
+                        torch.from_numpy(v).to(dev), eps=c.eps, dt=c.dt,
+                        integrator=os.environ.get("SWEEP_INTEGRATOR", "hermite"))
     sim.forces()
     sim.sync()
     sim.prof_enable(True)
@@ -72,8 +67,9 @@ def time_one(config, reps):
     sim.sync()
     chk = float(a.abs().sum().item() + j.abs().sum().item())
     t = ms / max(nf, 1)
+    fl = 40 if os.environ.get("SWEEP_INTEGRATOR", "hermite") == "hermite" else 18
     return {"ms": t, "interactions_per_s": c.n * c.n / (t * 1e-3),
-            "tflops40": 40 * c.n * c.n / (t * 1e-3) / 1e12, "checksum": chk}
+            "tflops": fl * c.n * c.n / (t * 1e-3) / 1e12, "checksum": chk}
 
 
 def run(config, reps):
