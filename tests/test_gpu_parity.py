@@ -198,7 +198,8 @@ def run_oracle_traj(m, x, v, eps, dt, nsteps, every):
     return states
 
 
-@pytest.mark.parametrize("cfg,every,dx_tol,dv_tol", [("C1", 1, 1e-9, 1e-6), ("C2", 10, 1e-6, 1e-4)])
+@pytest.mark.parametrize("cfg,every,dx_tol,dv_tol", [("C1", 1, 1e-9, 1e-6), ("C2", 10, 1e-6, 1e-4),
+                                                    ("C3", 5, 1e-6, 1e-4)])
 def test_trajectory_and_energy_drift(cfg, every, dx_tol, dv_tol):
     """R#14/R#15: same fp32 IC, Hermite P(EC)^1 on both sides; trajectory deltas and
     drift D = max_k |E_k - E_0| / |E_0| with both energies from the oracle."""
@@ -214,7 +215,7 @@ def test_trajectory_and_energy_drift(cfg, every, dx_tol, dv_tol):
     dx = np.linalg.norm(g[-1][0] - o[-1][0], axis=0)
     dv = np.linalg.norm(g[-1][1] - o[-1][1], axis=0)
     assert dx.max() <= dx_tol and dv.max() <= dv_tol, (dx.max(), dv.max())
-    if cfg == "C2":
+    if cfg != "C1":
         assert np.median(dx) <= 1e-9
     # momentum: sum m v stays at its initial value
     p0 = v @ m
