@@ -222,6 +222,9 @@ __global__ void __launch_bounds__(kThreads, kJerk ? FK_MINB : FK_MINB_ACC) force
         mbar_wait(&full[s], (uint32_t)((t / kStages) & 1));
         const JPkt* tile = ring + s * kTile;
         const float4* tile_lo = ring_lo + s * kTile;
+#if defined(FK_EXP_NOLDS) && !NB_PKT_DUP
+        float4 Pr = tile[0].p, Vr = tile[0].v;
+#endif
 
         f2 acc[kNC][kPairs];
 #pragma unroll
@@ -244,8 +247,21 @@ __global__ void __launch_bounds__(kThreads, kJerk ? FK_MINB : FK_MINB_ACC) force
             }
             const float jmass = tile[jj].b.z;
 #else
+#ifdef FK_EXP_NOLDS   // timing experiment only: j data from registers, perturbed by ALU ops
+            Pr.x = __int_as_float(__float_as_int(Pr.x) + 1);
+            Pr.y = __int_as_float(__float_as_int(Pr.y) + 1);
+            Pr.z = __int_as_float(__float_as_int(Pr.z) + 1);
+            Pr.w = __int_as_float(__float_as_int(Pr.w) + 1);
+            Vr.x = __int_as_float(__float_as_int(Vr.x) + 1);
+            Vr.y = __int_as_float(__float_as_int(Vr.y) + 1);
+            Vr.z = __int_as_float(__float_as_int(Vr.z) + 1);
+            Vr.w = __int_as_float(__float_as_int(Vr.w) + 1);
+            const float4 P = Pr;
+            const float4 V = Vr;
+#else
             const float4 P = tile[jj].p;
             const float4 V = tile[jj].v;
+#endif
             const f2 xj = f2bc(P.x), yj = f2bc(P.y), zj = f2bc(P.z), mj = f2bc(P.w);
             const f2 eps2 = f2bc(V.w);
             const f2 vxj = f2bc(V.x), vyj = f2bc(V.y), vzj = f2bc(V.z);
@@ -271,7 +287,12 @@ __global__ void __launch_bounds__(kThreads, kJerk ? FK_MINB : FK_MINB_ACC) force
                 s2 = ffma2(dz, dz, s2);
                 float s_lo, s_hi;
                 f2split(s2, s_lo, s_hi);
+#ifdef FK_EXP_NOMUFU  // timing experiment only
+                float r_lo = s_lo, r_hi = s_hi;
+                asm volatile("" : "+f"(r_lo), "+f"(r_hi));
+#else
                 float r_lo = rsqrt_ftz(s_lo), r_hi = rsqrt_ftz(s_hi);
+#endif
                 if (kGuard) {  // eps == 0: exclude j == i (s == 0), R#17
                     const int64_t jg = jc0 + (int64_t)t * kTile + jj;
                     if (s_lo == 0.f) {

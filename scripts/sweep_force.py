@@ -15,12 +15,9 @@ sys.path.insert(0, ROOT)
 OUT = os.path.join(ROOT, "scripts", "sweep")
 
 VARIANTS = {
-    "lf_b2":    dict(FK_MINB_ACC=2),
-    "lf_b3":    dict(FK_MINB_ACC=3),
-    "lf_b3u4":  dict(FK_MINB_ACC=3, FK_UNROLL=4),
-    "lf_b4p2":  dict(FK_MINB_ACC=4, FK_PAIRS=2, FK_MINB=3),
-    "lf_b3p3":  dict(FK_MINB_ACC=3, FK_PAIRS=3, FK_MINB=2),
-    "lf_b2p5":  dict(FK_MINB_ACC=2, FK_PAIRS=5, FK_MINB=2),
+    "base":     dict(),
+    "x_nolds":  dict(FK_EXP_NOLDS=1),
+    "x_both":   dict(FK_EXP_NOLDS=1, FK_EXP_NOMUFU=1),
 }
 if os.environ.get("SWEEP_ONLY"):
     VARIANTS = {k: v for k, v in VARIANTS.items() if k in os.environ["SWEEP_ONLY"].split(",")}

@@ -28,6 +28,9 @@ __global__ void __launch_bounds__(256) kern(float* out, float b, float c, unsign
         a[k] = threadIdx.x * 1e-3f + k;
         asm("mov.b64 %0, {%1, %2};" : "=l"(p[k]) : "f"(a[k]), "f"(a[k] + 1.f));
     }
+    double dd[CHAINS];
+    const double db = 0.999999;
+    for (int k = 0; k < CHAINS; ++k) dd[k] = k + threadIdx.x * 1e-3;
     unsigned long long q[CHAINS], r[CHAINS];
     float qs[CHAINS], rs[CHAINS];
     for (int k = 0; k < CHAINS; ++k) {
@@ -89,6 +92,23 @@ __global__ void __launch_bounds__(256) kern(float* out, float b, float c, unsign
                         a[k] = t.x;   // consume without FMA-pipe work (MODE 15)
                     }
                 }
+            } else if (MODE == 16) {  // DFMA only
+                asm volatile("fma.rn.f64 %0, %0, %1, %1;" : "+d"(dd[k]) : "d"(db));
+            } else if (MODE == 17) {  // FFMA2 + DFMA 1:1 (independent chains)
+                asm volatile("fma.rn.ftz.f32x2 %0, %0, %1, %2;" : "+l"(p[k]) : "l"(bb), "l"(cc));
+                asm volatile("fma.rn.f64 %0, %0, %1, %1;" : "+d"(dd[k]) : "d"(db));
+            } else if (MODE == 18) {  // FFMA2 + DFMA 2:1
+                asm volatile("fma.rn.ftz.f32x2 %0, %0, %1, %2;" : "+l"(p[k]) : "l"(bb), "l"(cc));
+                if (k & 1) asm volatile("fma.rn.f64 %0, %0, %1, %1;" : "+d"(dd[k]) : "d"(db));
+            } else if (MODE == 19) {  // FFMA2 / FMUL2 / FADD2 round robin (independent chains)
+                if (k % 3 == 0) asm volatile("fma.rn.ftz.f32x2 %0, %0, %1, %2;" : "+l"(p[k]) : "l"(bb), "l"(cc));
+                if (k % 3 == 1) asm volatile("mul.rn.ftz.f32x2 %0, %0, %1;" : "+l"(p[k]) : "l"(bb));
+                if (k % 3 == 2) asm volatile("add.rn.ftz.f32x2 %0, %0, %1;" : "+l"(p[k]) : "l"(cc));
+            } else if (MODE == 20) {  // the force loop's dependency shape: 3-deep FFMA2 chains x 8, + MUFU per 13
+                unsigned long long t1, t2;
+                asm volatile("add.rn.ftz.f32x2 %0, %1, %2;" : "=l"(t1) : "l"(p[k]), "l"(q[k]));
+                asm volatile("fma.rn.ftz.f32x2 %0, %1, %1, %2;" : "=l"(t2) : "l"(t1), "l"(cc));
+                asm volatile("fma.rn.ftz.f32x2 %0, %1, %2, %0;" : "+l"(p[k]) : "l"(t2), "l"(bb));
             } else if (MODE == 9) {  // scalar FFMA, three distinct registers
                 asm volatile("fma.rn.ftz.f32 %0, %1, %2, %0;" : "+f"(a[k]) : "f"(qs[k]), "f"(rs[k]));
             }
@@ -100,7 +120,7 @@ __global__ void __launch_bounds__(256) kern(float* out, float b, float c, unsign
     for (int k = 0; k < CHAINS; ++k) {
         float lo, hi;
         asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(p[k]));
-        s += a[k] + lo + hi;
+        s += a[k] + lo + hi + (float)dd[k];
     }
     if (s == 12345.f) out[0] = s;
     if (threadIdx.x == 0 && blockIdx.x == 0) {
@@ -110,12 +130,12 @@ __global__ void __launch_bounds__(256) kern(float* out, float b, float c, unsign
 }
 
 template <int MODE>
-void run(const char* name, double lane_ops_per_inst, int sms) {
+void run(const char* name, double lane_ops_per_inst, int sms, int bps = 8) {
     float* out;
     unsigned long long* clk;
     cudaMalloc(&out, 4);
     cudaMalloc(&clk, 16);
-    const int blocks = sms * 8, threads = 256;
+    const int blocks = sms * bps, threads = 256;
     kern<MODE><<<blocks, threads>>>(out, 0.999f, 1e-3f, clk);
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
@@ -132,8 +152,8 @@ void run(const char* name, double lane_ops_per_inst, int sms) {
     // lane_ops_per_inst = FP32 lane-ops per chain per iteration (MUFU counted only in mode 3)
     const double lane_ops = (double)blocks * threads * kIters * CHAINS * lane_ops_per_inst;
     const double per_sm_clk = lane_ops / (ms * 1e-3) / sms / (ghz * 1e9);
-    printf("%-28s %8.3f ms  clock %.3f GHz  %7.2f lane-ops/clk/SM  (%.2f T lane-ops/s)\n", name, ms,
-           ghz, per_sm_clk, lane_ops / (ms * 1e-3) / 1e12);
+    printf("%-28s bps=%d %8.3f ms  clock %.3f GHz  %7.2f lane-ops/clk/SM  (%.2f T lane-ops/s)\n", name, ms,
+           bps, ghz, per_sm_clk, lane_ops / (ms * 1e-3) / 1e12);
     cudaFree(out);
     cudaFree(clk);
 }
@@ -158,5 +178,15 @@ int main() {
     run<13>("FFMA2 4 : 1 LDS.128 (+2 FADD)", 2.0, sms);
     run<14>("FFMA2 4 : 1 LDS.64 (+1 FADD)", 2.0, sms);
     run<15>("FFMA2 8 : 1 LDS.128 (no use)", 2.0, sms);
+    run<16>("DFMA (fp64 lanes)", 1.0, sms);
+    run<17>("FFMA2 + DFMA 1:1 (fp32 lanes)", 2.0, sms);
+    run<18>("FFMA2 + DFMA 2:1 (fp32 lanes)", 2.0, sms);
+    run<19>("FFMA2/FMUL2/FADD2 mix", 2.0, sms);
+    run<20>("FADD2->FFMA2->FFMA2 chains", 6.0, sms);
+    for (int b : {1, 2, 3}) {
+        run<1>("FFMA2 (packed)", 2.0, sms, b);
+        run<20>("FADD2->FFMA2->FFMA2 chains", 6.0, sms, b);
+        run<4>("FFMA2 + MUFU 4:1 (FFMA2 lanes)", 2.0, sms, b);
+    }
     return 0;
 }
