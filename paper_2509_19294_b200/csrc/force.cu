@@ -42,6 +42,9 @@ namespace {
 #ifndef FK_MINB
 #define FK_MINB 2
 #endif
+#ifndef FK_RCP
+#define FK_RCP 0
+#endif
 #ifndef FK_MINB_ACC
 #define FK_MINB_ACC 2    // acceleration-only kernel (leapfrog)
 #endif
@@ -92,6 +95,11 @@ __device__ __forceinline__ f2 ffma2(f2 a, f2 b, f2 c) {
     f2 d;
     asm("fma.rn.ftz.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
     return d;
+}
+__device__ __forceinline__ float rcp_ftz(float s) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(s));
+    return r;
 }
 __device__ __forceinline__ float rsqrt_ftz(float s) {
     float r;
@@ -309,7 +317,12 @@ __global__ void __launch_bounds__(kThreads, kJerk ? FK_MINB : FK_MINB_ACC) force
                     }
                 }
                 const f2 ri = f2make(r_lo, r_hi);
+#if FK_RCP   // 1/s from MUFU.RCP (XU pipe) instead of ri * ri on the FMA pipe
+                f2 ri2 = f2make(rcp_ftz(s_lo), rcp_ftz(s_hi));
+                if (kGuard) ri2 = fmul2(ri, ri);
+#else
                 const f2 ri2 = fmul2(ri, ri);
+#endif
                 const f2 mr3 = fmul2(fmul2(mj, ri), ri2);      // G m_j / s^{3/2}
                 acc[0][p] = ffma2(mr3, dx, acc[0][p]);
                 acc[1][p] = ffma2(mr3, dy, acc[1][p]);
@@ -366,15 +379,34 @@ __global__ void __launch_bounds__(kThreads, kJerk ? FK_MINB : FK_MINB_ACC) force
 
 int force_i_per_block() { return kIPerBlock; }
 
+
+template <bool G, bool J, bool H>
+cudaError_t set_attr() {
+    return cudaFuncSetAttribute(force_kernel<G, J, H>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                kSmemBytes);
+}
+
+// dynamic shared memory above 48 KiB must be opted into once per instantiation
+cudaError_t ensure_attrs() {
+    static cudaError_t done = [] {
+        cudaError_t e = cudaSuccess, r;
+        if ((r = set_attr<false, false, false>()) != cudaSuccess) e = r;
+        if ((r = set_attr<false, false, true>()) != cudaSuccess) e = r;
+        if ((r = set_attr<false, true, false>()) != cudaSuccess) e = r;
+        if ((r = set_attr<false, true, true>()) != cudaSuccess) e = r;
+        if ((r = set_attr<true, false, false>()) != cudaSuccess) e = r;
+        if ((r = set_attr<true, false, true>()) != cudaSuccess) e = r;
+        if ((r = set_attr<true, true, false>()) != cudaSuccess) e = r;
+        if ((r = set_attr<true, true, true>()) != cudaSuccess) e = r;
+        return e;
+    }();
+    return done;
+}
+
 template <bool G, bool J, bool H>
 cudaError_t launch_one(const ForceArgs& a, dim3 grid, cudaStream_t s) {
-    static bool attr_set = false;   // per instantiation
-    if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(force_kernel<G, J, H>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
-        if (e != cudaSuccess) return e;
-        attr_set = true;
-    }
+    cudaError_t e = ensure_attrs();
+    if (e != cudaSuccess) return e;
     force_kernel<G, J, H><<<grid, kThreads, kSmemBytes, s>>>(a);
     return cudaGetLastError();
 }
@@ -390,6 +422,26 @@ cudaError_t launch_force(const ForceArgs& a, bool guard_self, bool jerk, cudaStr
     if (jerk)
         return guard_self ? launch_gj<true, true>(a, grid, s) : launch_gj<false, true>(a, grid, s);
     return guard_self ? launch_gj<true, false>(a, grid, s) : launch_gj<false, false>(a, grid, s);
+}
+
+int force_ctas_per_sm(bool jerk, bool hilo) {
+    int n = 0;
+    cudaError_t e = ensure_attrs();
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return FK_MINB;
+    }
+    if (jerk)
+        e = hilo ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, force_kernel<false, true, true>, kThreads, kSmemBytes)
+                 : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, force_kernel<false, true, false>, kThreads, kSmemBytes);
+    else
+        e = hilo ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, force_kernel<false, false, true>, kThreads, kSmemBytes)
+                 : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, force_kernel<false, false, false>, kThreads, kSmemBytes);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return FK_MINB;
+    }
+    return n > 0 ? n : 1;
 }
 
 }  // namespace nb

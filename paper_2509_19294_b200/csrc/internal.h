@@ -73,6 +73,8 @@ struct ForceArgs {
 // (leapfrog, NEXT f1; partial has 3 components).  Returns the launch error.
 cudaError_t launch_force(const ForceArgs& a, bool guard_self, bool jerk, cudaStream_t s);
 int force_i_per_block();
+// resident force CTAs per SM for the kernel variant (occupancy calculator)
+int force_ctas_per_sm(bool jerk, bool hilo);
 
 // fp64 particle-update kernels (hermite.cu).
 struct StateArgs {

@@ -123,6 +123,7 @@ bool is_device_ptr(const void* p) {
 struct nbody_ctx {
     nbody_config cfg{};
     int64_t n = 0, L = 0;
+    int sm_count = 148;
     float eps2f = 0.f;
     int nshards = 1;
     std::vector<Shard> sh;
@@ -268,10 +269,23 @@ int exchange_and_force(nbody_ctx* c) {
                                        c->comm_stream));
         }
         CK(c, cudaEventRecord(c->ev_gathered, c->comm_stream));
-        if ((rc = launch_force_range(c, s, s.c_lo, s.c_hi - s.c_lo))) return rc;
+        // Overlap: while the all-gather runs, compute a whole number of waves of
+        // local-chunk work items (i-block x chunk) -- a partial wave here would
+        // idle SMs until the launch drains, costing more than the ~10 us gather.
+        // Everything else (remaining local + all remote chunks) runs as one grid
+        // after the gather.  Results do not depend on this split.
+        const int32_t nl = s.c_hi - s.c_lo;
+        const int64_t n_ib = (s.n_loc + nb::force_i_per_block() - 1) / nb::force_i_per_block();
+        int32_t f = 0;
+        if (nl > 0 && n_ib > 0) {
+            const int64_t slots = (int64_t)c->sm_count * nb::force_ctas_per_sm(
+                                      c->cfg.integrator == NBODY_HERMITE4, c->pklo != nullptr);
+            f = (int32_t)std::min<int64_t>(nl, std::max<int64_t>(1, slots / n_ib));   // <= 1 wave
+        }
+        if ((rc = launch_force_range(c, s, s.c_lo, f))) return rc;
         CK(c, cudaStreamWaitEvent(c->stream, c->ev_gathered, 0));
-        const int32_t nrem = (int32_t)s.plan.n_chunks - (s.c_hi - s.c_lo);
-        if ((rc = launch_force_range(c, s, s.c_hi % (int32_t)s.plan.n_chunks, nrem))) return rc;
+        const int32_t nch = (int32_t)s.plan.n_chunks;
+        if ((rc = launch_force_range(c, s, (s.c_lo + f) % nch, nch - f))) return rc;
     } else {
         // world == 1 or loopback: every packet already sits in c->pkt
         for (auto& s : c->sh)
@@ -399,6 +413,7 @@ int init_impl(const nbody_config* cfg, const double* m, const double* x, const d
     c->L = std::max<int64_t>((int64_t)k.world * p0.slot, p0.n_chunks * p0.chunk);
 
     CK(c, cudaSetDevice(k.device));
+    CK(c, cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, k.device));
     if (k.stream) {
         c->stream = (cudaStream_t)k.stream;
     } else {

@@ -16,8 +16,7 @@ OUT = os.path.join(ROOT, "scripts", "sweep")
 
 VARIANTS = {
     "base":     dict(),
-    "x_nolds":  dict(FK_EXP_NOLDS=1),
-    "x_both":   dict(FK_EXP_NOLDS=1, FK_EXP_NOMUFU=1),
+    "rcp":      dict(FK_RCP=1),
 }
 if os.environ.get("SWEEP_ONLY"):
     VARIANTS = {k: v for k, v in VARIANTS.items() if k in os.environ["SWEEP_ONLY"].split(",")}
