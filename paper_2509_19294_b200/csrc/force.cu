@@ -45,6 +45,12 @@ namespace {
 #ifndef FK_RCP
 #define FK_RCP 0
 #endif
+#ifndef FK_HYB
+#define FK_HYB 0         // fp64 i-particles per thread on the FP64 pipe (measured slower; 0: off)
+#endif
+#ifndef FK_HYB_NEWTON
+#define FK_HYB_NEWTON 1  // Newton step after rsqrt.approx.f64
+#endif
 #ifndef FK_MINB_ACC
 #define FK_MINB_ACC 2    // acceleration-only kernel (leapfrog)
 #endif
@@ -59,13 +65,16 @@ constexpr int kThreads = FK_THREADS;
 constexpr int kPairs = FK_PAIRS;          // i-pairs per thread (2 * kPairs i)
 constexpr int kStages = FK_STAGES;        // smem ring depth (tiles)
 constexpr int kUnroll = FK_UNROLL;
-constexpr int kIPerBlock = 2 * kPairs * kThreads;
+constexpr int kHyb = FK_HYB;              // fp64 i per thread (FP64 pipe, runs beside FFMA2)
+constexpr int kIPerBlock = (2 * kPairs + kHyb) * kThreads;
 constexpr int kTileBytes = kTile * (int)sizeof(JPkt);
 constexpr int kLoTileBytes = kTile * (int)sizeof(float4);   // hi/lo position tails (NEXT f2)
+constexpr int kT64TileBytes = kHyb ? kTile * (int)sizeof(JPkt64) : 0;   // fp64 j tiles
 constexpr int kAccSmemBytes = FK_ACC_SMEM ? 6 * 2 * kPairs * kThreads * 8 : 0;
 // shared memory layout: [ring: kStages j-tiles][ring_lo: kStages lo-tiles][64 B mbarriers][fp64 acc]
 constexpr int kOffLo = kStages * kTileBytes;
-constexpr int kOffBar = kOffLo + kStages * kLoTileBytes;
+constexpr int kOff64 = kOffLo + kStages * kLoTileBytes;
+constexpr int kOffBar = kOff64 + kStages * kT64TileBytes;
 constexpr int kOffAcc = kOffBar + 64;
 constexpr int kSmemBytes = kOffAcc + kAccSmemBytes;
 static_assert(kStages * 8 <= 64, "mbarrier area");
@@ -96,7 +105,12 @@ __device__ __forceinline__ f2 ffma2(f2 a, f2 b, f2 c) {
     asm("fma.rn.ftz.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
     return d;
 }
-__device__ __forceinline__ float rcp_ftz(float s) {
+__device__ __forceinline__ double rsqrt_approx_f64(double s) {
+    double r;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(s));   // MUFU.RSQ64H, no slow path
+    return r;
+}
+[[maybe_unused]] __device__ __forceinline__ float rcp_ftz(float s) {
     float r;
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(s));
     return r;
@@ -144,10 +158,11 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t
 template <bool kGuard, bool kJerk, bool kHiLo>
 __global__ void __launch_bounds__(kThreads, kJerk ? FK_MINB : FK_MINB_ACC) force_kernel(ForceArgs a) {
     constexpr int kNC = kJerk ? 6 : 3;   // accumulated components: a (+ jerk)
-    constexpr uint32_t kStageTx = kTileBytes + (kHiLo ? kLoTileBytes : 0);
+    constexpr uint32_t kStageTx = kTileBytes + (kHiLo ? kLoTileBytes : 0) + kT64TileBytes;
     extern __shared__ __align__(128) unsigned char smem[];
     JPkt* ring = reinterpret_cast<JPkt*>(smem);
     float4* ring_lo = reinterpret_cast<float4*>(smem + kOffLo);
+    JPkt64* ring64 = reinterpret_cast<JPkt64*>(smem + kOff64);
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + kOffBar);
 
     const int tid = threadIdx.x;
@@ -194,6 +209,25 @@ __global__ void __launch_bounds__(kThreads, kJerk ? FK_MINB : FK_MINB_ACC) force
         }
     }
 
+    // ---- fp64 i-particles (slots 2*kPairs .. 2*kPairs+kHyb-1 of the thread): exact fp64
+    //      state, interactions on the FP64 pipe, accumulated in fp64 over the chunk
+    double hx[kHyb > 0 ? kHyb : 1], hy[kHyb > 0 ? kHyb : 1], hz[kHyb > 0 ? kHyb : 1];
+    double hvx[kHyb > 0 ? kHyb : 1], hvy[kHyb > 0 ? kHyb : 1], hvz[kHyb > 0 ? kHyb : 1];
+    double hacc[kNC][kHyb > 0 ? kHyb : 1];
+#pragma unroll
+    for (int h = 0; h < kHyb; ++h) {
+        const int il = ib + (2 * kPairs + h) * kThreads + tid;
+        if (il < a.n_loc) {
+            const JPkt64 pk = a.pk64[a.i_base + il];
+            hx[h] = pk.p.x; hy[h] = pk.p.y; hz[h] = pk.p.z;
+            hvx[h] = pk.v.x; hvy[h] = pk.v.y; hvz[h] = pk.v.z;
+        } else {
+            hx[h] = hy[h] = hz[h] = hvx[h] = hvy[h] = hvz[h] = 0.0;
+        }
+#pragma unroll
+        for (int k = 0; k < kNC; ++k) hacc[k][h] = 0.0;
+    }
+
 #if FK_ACC_SMEM
     // fp64 chunk accumulators in shared memory: [k][l][tid], conflict-free
     double* acc_s = reinterpret_cast<double*>(smem + kOffAcc);
@@ -220,6 +254,9 @@ __global__ void __launch_bounds__(kThreads, kJerk ? FK_MINB : FK_MINB_ACC) force
             if (kHiLo)
                 tma_load_1d(ring_lo + s * kTile, a.pklo + jc0 + (int64_t)s * kTile, kLoTileBytes,
                             &full[s]);
+            if (kHyb)
+                tma_load_1d(ring64 + s * kTile, a.pk64 + jc0 + (int64_t)s * kTile, kT64TileBytes,
+                            &full[s]);
         }
     }
 
@@ -230,6 +267,7 @@ __global__ void __launch_bounds__(kThreads, kJerk ? FK_MINB : FK_MINB_ACC) force
         mbar_wait(&full[s], (uint32_t)((t / kStages) & 1));
         const JPkt* tile = ring + s * kTile;
         const float4* tile_lo = ring_lo + s * kTile;
+        const JPkt64* tile64 = ring64 + s * kTile;
 #if defined(FK_EXP_NOLDS) && !NB_PKT_DUP
         float4 Pr = tile[0].p, Vr = tile[0].v;
 #endif
@@ -340,6 +378,44 @@ __global__ void __launch_bounds__(kThreads, kJerk ? FK_MINB : FK_MINB_ACC) force
                     acc[5 % kNC][p] = ffma2(mr3, ffma2(q3, dz, wz), acc[5 % kNC][p]);
                 }
             }
+            // ---- the same interaction in fp64 for the thread's kHyb fp64 i-particles.
+            //      DADD/DFMA/DMUL issue to the FP64 pipe, which runs beside FFMA2
+            //      (scripts/ubench_fp32.cu: 4 FFMA2 : 3 DFMA keeps ~95 % of the FP32 rate).
+            if (kHyb) {
+                const double4 Pd = tile64[jj].p;   // x, y, z, G m
+                const double4 Vd = tile64[jj].v;   // vx, vy, vz, eps2
+#pragma unroll
+                for (int h = 0; h < kHyb; ++h) {
+                    const double dx = Pd.x - hx[h], dy = Pd.y - hy[h], dz = Pd.z - hz[h];
+                    const double s = fma(dz, dz, fma(dy, dy, fma(dx, dx, Vd.w)));
+                    double ri = rsqrt_approx_f64(s);
+#if FK_HYB_NEWTON
+                    ri = ri * fma(-0.5 * s, ri * ri, 1.5);
+#endif
+                    if (kGuard) {
+                        if (s == 0.0) {
+                            ri = 0.0;
+                            const int64_t ig = a.i_base + ib + (2 * kPairs + h) * kThreads + tid;
+                            const int64_t jg = jc0 + (int64_t)t * kTile + jj;
+                            if (ig != jg && ig < a.i_base + a.n_loc && Pd.w != 0.0)
+                                atomicMin(a.coincident, (unsigned long long)ig);
+                        }
+                    }
+                    const double ri2 = ri * ri;
+                    const double mr3 = Pd.w * ri * ri2;
+                    hacc[0][h] = fma(mr3, dx, hacc[0][h]);
+                    hacc[1][h] = fma(mr3, dy, hacc[1][h]);
+                    hacc[2][h] = fma(mr3, dz, hacc[2][h]);
+                    if (kJerk) {
+                        const double wx = Vd.x - hvx[h], wy = Vd.y - hvy[h], wz = Vd.z - hvz[h];
+                        const double rv = fma(dz, wz, fma(dy, wy, dx * wx));
+                        const double q3 = -3.0 * rv * ri2;
+                        hacc[3 % kNC][h] = fma(mr3, fma(q3, dx, wx), hacc[3 % kNC][h]);
+                        hacc[4 % kNC][h] = fma(mr3, fma(q3, dy, wy), hacc[4 % kNC][h]);
+                        hacc[5 % kNC][h] = fma(mr3, fma(q3, dz, wz), hacc[5 % kNC][h]);
+                    }
+                }
+            }
         }
         // tile sum -> fp64, ascending tile order
 #pragma unroll
@@ -359,6 +435,9 @@ __global__ void __launch_bounds__(kThreads, kJerk ? FK_MINB : FK_MINB_ACC) force
             if (kHiLo)
                 tma_load_1d(ring_lo + s * kTile, a.pklo + jc0 + (int64_t)(t + kStages) * kTile,
                             kLoTileBytes, &full[s]);
+            if (kHyb)
+                tma_load_1d(ring64 + s * kTile, a.pk64 + jc0 + (int64_t)(t + kStages) * kTile,
+                            kT64TileBytes, &full[s]);
         }
     }
 
@@ -372,12 +451,21 @@ __global__ void __launch_bounds__(kThreads, kJerk ? FK_MINB : FK_MINB_ACC) force
             for (int k = 0; k < kNC; ++k) out[(int64_t)k * a.n_loc_pad + il] = ACC64(k, l);
         }
     }
+#pragma unroll
+    for (int h = 0; h < kHyb; ++h) {
+        const int il = ib + (2 * kPairs + h) * kThreads + tid;
+        if (il < a.n_loc) {
+#pragma unroll
+            for (int k = 0; k < kNC; ++k) out[(int64_t)k * a.n_loc_pad + il] = hacc[k][h];
+        }
+    }
 #undef ACC64
 }
 
 }  // namespace
 
 int force_i_per_block() { return kIPerBlock; }
+int force_hyb() { return kHyb; }
 
 
 template <bool G, bool J, bool H>

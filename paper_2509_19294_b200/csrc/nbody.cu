@@ -89,7 +89,10 @@ int make_plan(int64_t n, int32_t world, int32_t rank, int32_t jchunks, Plan* p, 
     if (jchunks < 0) { *why = "jchunks must be >= 0"; return NBODY_EINVAL; }
     const int64_t jc = jchunks == 0 ? 128 : jchunks;
     const int64_t T = nb::kTile;
-    p->slot = T * ((n + T * world - 1) / (T * world));
+    // slot: multiple of the force i-block, so which arithmetic (FP32 pair lane or
+    // FP64 slot) a particle gets depends on its global index only (P-invariant)
+    const int64_t B = nb::force_i_per_block();
+    p->slot = B * ((n + B * world - 1) / (B * world));
     p->i0 = std::min<int64_t>(n, rank * p->slot);
     p->i1 = std::min<int64_t>(n, (int64_t)(rank + 1) * p->slot);
     p->chunk = T * ((n + T * jc - 1) / (T * jc));
@@ -129,6 +132,7 @@ struct nbody_ctx {
     std::vector<Shard> sh;
     JPkt* pkt = nullptr;
     float4* pklo = nullptr;   // hi/lo position tails (cfg.hilo)
+    nb::JPkt64* pk64 = nullptr;   // fp64 packets for the force kernel's FP64-pipe share
     double4* eall = nullptr;
     double* eblk = nullptr;
     int eblk_cap = 0;
@@ -207,6 +211,7 @@ nb::StateArgs state_args(nbody_ctx* c, Shard& s) {
     a.integrator = c->cfg.integrator;
     a.pkt = c->pkt;
     a.pklo = c->pklo;
+    a.pk64 = c->pk64;
     a.bad = c->flags;
     return a;
 }
@@ -218,6 +223,7 @@ int launch_force_range(nbody_ctx* c, Shard& s, int32_t c_first, int32_t c_count)
     nb::ForceArgs f;
     f.pkt = c->pkt;
     f.pklo = c->pklo;
+    f.pk64 = c->pk64;
     f.i_base = s.plan.i0;
     f.n_loc = s.n_loc;
     f.n_loc_pad = s.n_loc_pad;
@@ -266,6 +272,12 @@ int exchange_and_force(nbody_ctx* c) {
             float* lo = reinterpret_cast<float*>(c->pklo);
             const size_t cl = (size_t)s.plan.slot * 4;
             CKNCCL(c, nccl().AllGather(lo + (size_t)c->cfg.rank * cl, lo, cl, ncclFloat32, c->comm,
+                                       c->comm_stream));
+        }
+        if (c->pk64) {
+            double* d64 = reinterpret_cast<double*>(c->pk64);
+            const size_t c8 = (size_t)s.plan.slot * 8;
+            CKNCCL(c, nccl().AllGather(d64 + (size_t)c->cfg.rank * c8, d64, c8, ncclFloat64, c->comm,
                                        c->comm_stream));
         }
         CK(c, cudaEventRecord(c->ev_gathered, c->comm_stream));
@@ -360,6 +372,7 @@ void free_ctx(nbody_ctx* c) {
     }
     cudaFree(c->pkt);
     cudaFree(c->pklo);
+    cudaFree(c->pk64);
     cudaFree(c->eall);
     cudaFree(c->eblk);
     cudaFree(c->eout);
@@ -426,9 +439,10 @@ int init_impl(const nbody_config* cfg, const double* m, const double* x, const d
 
     if ((rc = dalloc(c, &c->pkt, (size_t)c->L))) return rc;
     if (k.hilo && (rc = dalloc(c, &c->pklo, (size_t)c->L))) return rc;
+    if (nb::force_hyb() > 0 && (rc = dalloc(c, &c->pk64, (size_t)c->L))) return rc;
     if ((rc = dalloc(c, &c->flags, 4))) return rc;
     CK(c, cudaMemsetAsync(c->flags, 0xff, 4 * sizeof(unsigned long long), c->stream));
-    CK(c, nb::launch_fill_padding(c->pkt, c->pklo, 0, c->L, c->eps2f, c->stream));
+    CK(c, nb::launch_fill_padding(c->pkt, c->pklo, c->pk64, 0, c->L, c->eps2f, c->stream));
     c->n_kernels++;
 
     const int64_t ib = nb::force_i_per_block();

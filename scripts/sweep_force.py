@@ -15,8 +15,15 @@ sys.path.insert(0, ROOT)
 OUT = os.path.join(ROOT, "scripts", "sweep")
 
 VARIANTS = {
-    "base":     dict(),
-    "rcp":      dict(FK_RCP=1),
+    "h0p4":    dict(FK_HYB=0, FK_PAIRS=4),
+    "h2p4":    dict(FK_HYB=2, FK_PAIRS=4),
+    "h1p4":    dict(FK_HYB=1, FK_PAIRS=4),
+    "h2p3":    dict(FK_HYB=2, FK_PAIRS=3),
+    "h3p3":    dict(FK_HYB=3, FK_PAIRS=3),
+    "h2p2":    dict(FK_HYB=2, FK_PAIRS=2),
+    "h2p3n0":  dict(FK_HYB=2, FK_PAIRS=3, FK_HYB_NEWTON=0),
+    "h2p4n0":  dict(FK_HYB=2, FK_PAIRS=4, FK_HYB_NEWTON=0),
+    "h1p3":    dict(FK_HYB=1, FK_PAIRS=3),
 }
 if os.environ.get("SWEEP_ONLY"):
     VARIANTS = {k: v for k, v in VARIANTS.items() if k in os.environ["SWEEP_ONLY"].split(",")}
@@ -62,10 +69,17 @@ def time_one(config, reps):
     a, j = sim.forces()
     sim.sync()
     chk = float(a.abs().sum().item() + j.abs().sum().item())
+    import oracle
+    idx = np.linspace(0, c.n - 1, 2048).astype(np.int64)
+    idx = np.unique(np.concatenate([idx, np.arange(1024, 1280), np.arange(768, 1024)]))
+    ao, jo = oracle.forces(m, x, v, float(np.float32(c.eps * c.eps)), idx=idx)
+    an, jn = a.cpu().numpy()[:, idx], j.cpu().numpy()[:, idx]
+    ea = float(np.max(np.linalg.norm(an - ao, axis=0) / np.linalg.norm(ao, axis=0)))
+    ej = float(np.max(np.linalg.norm(jn - jo, axis=0) / np.linalg.norm(jo, axis=0)))
     t = ms / max(nf, 1)
     fl = 40 if os.environ.get("SWEEP_INTEGRATOR", "hermite") == "hermite" else 18
     return {"ms": t, "interactions_per_s": c.n * c.n / (t * 1e-3),
-            "tflops": fl * c.n * c.n / (t * 1e-3) / 1e12, "checksum": chk}
+            "tflops": fl * c.n * c.n / (t * 1e-3) / 1e12, "checksum": chk, "err_a": ea, "err_j": ej}
 
 
 def run(config, reps):

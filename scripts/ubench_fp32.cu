@@ -109,6 +109,11 @@ __global__ void __launch_bounds__(256) kern(float* out, float b, float c, unsign
                 asm volatile("add.rn.ftz.f32x2 %0, %1, %2;" : "=l"(t1) : "l"(p[k]), "l"(q[k]));
                 asm volatile("fma.rn.ftz.f32x2 %0, %1, %1, %2;" : "=l"(t2) : "l"(t1), "l"(cc));
                 asm volatile("fma.rn.ftz.f32x2 %0, %1, %2, %0;" : "+l"(p[k]) : "l"(t2), "l"(bb));
+            } else if (MODE == 21) {  // 4 FFMA2 : 3 DFMA (hybrid force-loop ratio), independent
+                asm volatile("fma.rn.ftz.f32x2 %0, %0, %1, %2;" : "+l"(p[k]) : "l"(bb), "l"(cc));
+                if (k % 4 != 3) asm volatile("fma.rn.f64 %0, %0, %1, %1;" : "+d"(dd[k]) : "d"(db));
+            } else if (MODE == 22) {  // same FP32 work alone
+                asm volatile("fma.rn.ftz.f32x2 %0, %0, %1, %2;" : "+l"(p[k]) : "l"(bb), "l"(cc));
             } else if (MODE == 9) {  // scalar FFMA, three distinct registers
                 asm volatile("fma.rn.ftz.f32 %0, %1, %2, %0;" : "+f"(a[k]) : "f"(qs[k]), "f"(rs[k]));
             }
@@ -183,7 +188,11 @@ int main() {
     run<18>("FFMA2 + DFMA 2:1 (fp32 lanes)", 2.0, sms);
     run<19>("FFMA2/FMUL2/FADD2 mix", 2.0, sms);
     run<20>("FADD2->FFMA2->FFMA2 chains", 6.0, sms);
-    for (int b : {1, 2, 3}) {
+    for (int b : {1, 2, 8}) {
+        run<21>("4 FFMA2 : 3 DFMA (fp32 lanes)", 2.0, sms, b);
+        run<22>("FFMA2 alone (fp32 lanes)", 2.0, sms, b);
+    }
+    for (int b : {1}) {
         run<1>("FFMA2 (packed)", 2.0, sms, b);
         run<20>("FADD2->FFMA2->FFMA2 chains", 6.0, sms, b);
         run<4>("FFMA2 + MUFU 4:1 (FFMA2 lanes)", 2.0, sms, b);
