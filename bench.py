@@ -149,6 +149,9 @@ class EnergyMeter:
         t = time.perf_counter() - self.t0
         e1 = self._read()
         g = (e1[0] - self.e0[0]) if e1[0] is not None and self.e0[0] is not None else None
+        if g is not None and (t < 0.25 or g <= 0):   # below the counter's update granularity
+            return {"gpu_joules": None, "host_cpu_joules": None, "seconds": t, "gpu_avg_w": None,
+                    "note": "region shorter than the NVML energy counter resolution"}
         c = (e1[1] - self.e0[1]) if e1[1] is not None and self.e0[1] is not None else None
         return {"gpu_joules": g, "host_cpu_joules": c, "seconds": t,
                 "gpu_avg_w": g / t if g is not None and t > 0 else None}
