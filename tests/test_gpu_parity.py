@@ -322,3 +322,34 @@ def test_cuda_graph_replay_bit_identical(monkeypatch):
             st.synchronize()
             out.append((xs.cpu().numpy(), vs.cpu().numpy()))
     assert np.array_equal(out[0][0], out[1][0]) and np.array_equal(out[0][1], out[1][1])
+
+
+def test_c_abi_argument_errors():
+    """EINVAL paths of the C-ABI with a live context (messages name the problem)."""
+    m, x, v = inputs.make("C1")
+    L = binding.lib()
+    with binding.NBody(m, x, v, eps=1e-2, dt=1 / 1024) as s:
+        assert L.nbody_step(s._ctx, 0) == binding.NBODY_EINVAL
+        assert "nsteps" in L.nbody_last_error(s._ctx).decode()
+        xb = np.ascontiguousarray(x.copy())
+        xb[2, 900] = np.inf
+        with pytest.raises(binding.NBodyError, match="particle 900"):
+            s.set_state(xb, v)
+        # the context stays usable after a rejected set_state (not sticky)
+        s.set_state(x, v)
+        a, _ = s.forces()
+        s.sync()
+        ao, _ = oracle.forces(m, x, v, eps2_of(1e-2))
+        assert max_rel(a.cpu().numpy(), ao) <= TOL_ACC
+    L.nbody_destroy(None)   # no-op
+
+
+def test_get_state_partial_outputs_and_energy_consistency():
+    m, x, v = inputs.make("C1")
+    with binding.NBody(m, x, v, eps=1e-2, dt=1 / 1024) as s:
+        xs = np.empty((3, 1024))
+        binding._check(binding.lib().nbody_get_state(s._ctx, xs.ctypes.data, None), s._ctx)
+        assert np.array_equal(xs, x)       # init copies the state losslessly
+        ke1, pe1 = s.energy()
+        ke2, pe2 = s.energy()
+        assert (ke1, pe1) == (ke2, pe2)    # deterministic reduction
