@@ -299,6 +299,11 @@ def main():
     clk = clocks.stop()
     sim.sync()
     ms_steps = sum(a.elapsed_time(b) for a, b in ev)
+    if world > 1:   # whole-job GPU energy: sum over ranks (NaN marks a rank without a reading)
+        ej = torch.tensor([energy["gpu_joules"] if energy["gpu_joules"] is not None else float("nan")],
+                          dtype=torch.float64, device=dev)
+        dist.all_reduce(ej, op=dist.ReduceOp.SUM)
+        energy["gpu_joules"] = None if ej.isnan().item() else ej.item()
     _, _, launches = sim.prof_read(reset=True)
 
     # ---- pass B (roofline of the force kernel): the library brackets every force
@@ -412,7 +417,7 @@ def main():
                                                     if energy["gpu_joules"] is not None else None),
                            interactions_per_joule=(float(n) * n * args.steps / energy["gpu_joules"]
                                                    if energy["gpu_joules"] else None),
-                           scope="this rank's GPU (NVML total-energy counter) over the timed region"),
+                           scope=f"{world} GPU(s), NVML total-energy counter, summed over ranks, timed region"),
             "gpu_launches": launches,
             "e2e": e2e,
             "cpu_baseline": cpu,

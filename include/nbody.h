@@ -186,6 +186,13 @@ int nbody_prof_enable(nbody_ctx* ctx, int32_t on);
 int nbody_prof_read(nbody_ctx* ctx, double* force_ms, int64_t* force_launches,
                     int64_t* kernel_launches, int32_t reset);
 
+/* Per-launch force-kernel times (ms, launch order) recorded since the last
+ * reset while profiling was on: writes min(count, cap) values to ms and the
+ * total number recorded to *count.  Blocks.  In loopback mode the launches of
+ * shard s follow those of shard s - 1 within each evaluation, so per-shard
+ * (per-emulated-GPU) times can be read off (scripts/project_scaling.py). */
+int nbody_prof_launch_times(nbody_ctx* ctx, double* ms, int64_t cap, int64_t* count);
+
 /* Message for the last failure on ctx (or of the last failed nbody_init /
  * plan call when ctx is NULL).  Never NULL; valid until the next call. */
 const char* nbody_last_error(const nbody_ctx* ctx);

@@ -21,6 +21,7 @@ EXPORTS = (
     "nbody_plan", "nbody_nccl_unique_id", "nbody_init", "nbody_local_range",
     "nbody_compute_forces", "nbody_step", "nbody_energy", "nbody_get_state",
     "nbody_set_state", "nbody_sync", "nbody_prof_enable", "nbody_prof_read",
+    "nbody_prof_launch_times",
     "nbody_last_error", "nbody_destroy",
 )
 
@@ -90,6 +91,7 @@ def lib():
         "nbody_sync": ([p], ctypes.c_int),
         "nbody_prof_enable": ([p, i32], ctypes.c_int),
         "nbody_prof_read": ([p, Pd, P64, P64, i32], ctypes.c_int),
+        "nbody_prof_launch_times": ([p, p, i64, P64], ctypes.c_int),
         "nbody_last_error": ([p], ctypes.c_char_p),
         "nbody_destroy": ([p], None),
     }
@@ -230,6 +232,14 @@ class NBody:
         self._c(lib().nbody_prof_read(self._ctx, ctypes.byref(ms), ctypes.byref(nf),
                                       ctypes.byref(nk), 1 if reset else 0))
         return ms.value, nf.value, nk.value
+
+    def prof_launch_times(self):
+        """Per-launch force-kernel times (ms) since the last prof_read(reset=True)."""
+        n = ctypes.c_int64()
+        self._c(lib().nbody_prof_launch_times(self._ctx, None, 0, ctypes.byref(n)))
+        out = np.zeros(n.value)
+        self._c(lib().nbody_prof_launch_times(self._ctx, out.ctypes.data, n.value, ctypes.byref(n)))
+        return out
 
     def close(self):
         if getattr(self, "_ctx", None):

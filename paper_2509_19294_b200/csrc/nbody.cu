@@ -737,6 +737,19 @@ int nbody_prof_read(nbody_ctx* c, double* force_ms, int64_t* force_launches, int
     return NBODY_OK;
 }
 
+int nbody_prof_launch_times(nbody_ctx* c, double* ms, int64_t cap, int64_t* count) {
+    GUARD(c);
+    CK(c, cudaStreamSynchronize(c->stream));
+    const int64_t nrec = (int64_t)(c->prof_used / 2);
+    for (int64_t q = 0; q < nrec && q < cap && ms; ++q) {
+        float t = 0;
+        CK(c, cudaEventElapsedTime(&t, c->prof_ev[2 * q], c->prof_ev[2 * q + 1]));
+        ms[q] = t;
+    }
+    if (count) *count = nrec;
+    return NBODY_OK;
+}
+
 const char* nbody_last_error(const nbody_ctx* c) {
     if (c) return c->err.c_str();
     return g_last_error.c_str();

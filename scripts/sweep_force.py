@@ -15,15 +15,12 @@ sys.path.insert(0, ROOT)
 OUT = os.path.join(ROOT, "scripts", "sweep")
 
 VARIANTS = {
-    "h0p4":    dict(FK_HYB=0, FK_PAIRS=4),
-    "h2p4":    dict(FK_HYB=2, FK_PAIRS=4),
-    "h1p4":    dict(FK_HYB=1, FK_PAIRS=4),
-    "h2p3":    dict(FK_HYB=2, FK_PAIRS=3),
-    "h3p3":    dict(FK_HYB=3, FK_PAIRS=3),
-    "h2p2":    dict(FK_HYB=2, FK_PAIRS=2),
-    "h2p3n0":  dict(FK_HYB=2, FK_PAIRS=3, FK_HYB_NEWTON=0),
-    "h2p4n0":  dict(FK_HYB=2, FK_PAIRS=4, FK_HYB_NEWTON=0),
-    "h1p3":    dict(FK_HYB=1, FK_PAIRS=3),
+    "base":      dict(),
+    "t64b4":     dict(FK_THREADS=64, FK_MINB=4),
+    "t256b1":    dict(FK_THREADS=256, FK_MINB=1),
+    "u3":        dict(FK_UNROLL=3),
+    "st3":       dict(FK_STAGES=3),
+    "st4u1":     dict(FK_STAGES=4, FK_UNROLL=1),
 }
 if os.environ.get("SWEEP_ONLY"):
     VARIANTS = {k: v for k, v in VARIANTS.items() if k in os.environ["SWEEP_ONLY"].split(",")}
