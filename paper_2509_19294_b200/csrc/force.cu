@@ -60,6 +60,12 @@ namespace {
 #ifndef FK_ACC_SMEM
 #define FK_ACC_SMEM 1
 #endif
+#ifndef FK_PREFETCH
+#define FK_PREFETCH 0    // 1: j packet of the next j loaded into registers one iteration ahead
+#endif
+#ifndef FK_EMPTYBAR
+#define FK_EMPTYBAR 0    // 1: per-stage "empty" mbarriers (one arrive per warp) instead of a CTA barrier per tile
+#endif
 
 constexpr int kThreads = FK_THREADS;
 constexpr int kPairs = FK_PAIRS;          // i-pairs per thread (2 * kPairs i)
@@ -77,7 +83,8 @@ constexpr int kOff64 = kOffLo + kStages * kLoTileBytes;
 constexpr int kOffBar = kOff64 + kStages * kT64TileBytes;
 constexpr int kOffAcc = kOffBar + 64;
 constexpr int kSmemBytes = kOffAcc + kAccSmemBytes;
-static_assert(kStages * 8 <= 64, "mbarrier area");
+static_assert(kStages * 8 * (FK_EMPTYBAR ? 2 : 1) <= 64, "mbarrier area");
+static_assert(!FK_EMPTYBAR || (kStages >= 3 && kHyb == 0), "empty-barrier ring: >= 3 stages, no fp64 share");
 
 typedef unsigned long long f2;  // packed {lo, hi} fp32 pair in one 64-bit register
 
@@ -145,6 +152,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
             : "memory");
     }
 }
+[[maybe_unused]] __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
 // 1-D bulk TMA global -> shared, completion counted on `bar` (UBLKCP in SASS)
 __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes,
                                             uint64_t* bar) {
@@ -164,6 +174,7 @@ __global__ void __launch_bounds__(kThreads, kJerk ? FK_MINB : FK_MINB_ACC) force
     float4* ring_lo = reinterpret_cast<float4*>(smem + kOffLo);
     JPkt64* ring64 = reinterpret_cast<JPkt64*>(smem + kOff64);
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + kOffBar);
+    [[maybe_unused]] uint64_t* empty = full + kStages;   // FK_EMPTYBAR: all warps done with a stage
 
     const int tid = threadIdx.x;
     const int c = (a.c_first + (int)blockIdx.y) % a.n_chunks;
@@ -244,6 +255,9 @@ __global__ void __launch_bounds__(kThreads, kJerk ? FK_MINB : FK_MINB_ACC) force
     if (tid == 0) {
 #pragma unroll
         for (int s = 0; s < kStages; ++s) mbar_init(&full[s], 1);
+#if FK_EMPTYBAR
+        for (int s = 0; s < kStages; ++s) mbar_init(&empty[s], kThreads / 32);
+#endif
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
@@ -270,6 +284,9 @@ __global__ void __launch_bounds__(kThreads, kJerk ? FK_MINB : FK_MINB_ACC) force
         const JPkt64* tile64 = ring64 + s * kTile;
 #if defined(FK_EXP_NOLDS) && !NB_PKT_DUP
         float4 Pr = tile[0].p, Vr = tile[0].v;
+#endif
+#if FK_PREFETCH && !NB_PKT_DUP && !defined(FK_EXP_NOLDS)
+        float4 Pn = tile[0].p, Vn = tile[0].v;
 #endif
 
         f2 acc[kNC][kPairs];
@@ -305,8 +322,17 @@ __global__ void __launch_bounds__(kThreads, kJerk ? FK_MINB : FK_MINB_ACC) force
             const float4 P = Pr;
             const float4 V = Vr;
 #else
+#if FK_PREFETCH
+            const float4 P = Pn, V = Vn;
+            {
+                const int jn = jj + 1 < kTile ? jj + 1 : jj;   // stays inside the stage
+                Pn = tile[jn].p;
+                Vn = tile[jn].v;
+            }
+#else
             const float4 P = tile[jj].p;
             const float4 V = tile[jj].v;
+#endif
 #endif
             const f2 xj = f2bc(P.x), yj = f2bc(P.y), zj = f2bc(P.z), mj = f2bc(P.w);
             const f2 eps2 = f2bc(V.w);
@@ -427,6 +453,22 @@ __global__ void __launch_bounds__(kThreads, kJerk ? FK_MINB : FK_MINB_ACC) force
                 ACC64(k, 2 * p) += (double)lo;
                 ACC64(k, 2 * p + 1) += (double)hi;
             }
+#if FK_EMPTYBAR
+        // each warp releases stage s; thread 0 refills the stage released one tile
+        // earlier (t - 1), so only warp 0 waits, and only for the slowest warp's tile t - 1
+        __syncwarp();
+        if ((tid & 31) == 0) mbar_arrive(&empty[s]);
+        if (tid == 0 && t >= 1 && t - 1 + kStages < ntile) {
+            const int sp = (t - 1) % kStages;
+            mbar_wait(&empty[sp], (uint32_t)(((t - 1) / kStages) & 1));
+            mbar_expect_tx(&full[sp], kStageTx);
+            tma_load_1d(ring + sp * kTile, a.pkt + jc0 + (int64_t)(t - 1 + kStages) * kTile,
+                        kTileBytes, &full[sp]);
+            if (kHiLo)
+                tma_load_1d(ring_lo + sp * kTile, a.pklo + jc0 + (int64_t)(t - 1 + kStages) * kTile,
+                            kLoTileBytes, &full[sp]);
+        }
+#else
         __syncthreads();  // every warp is done reading stage s
         if (tid == 0 && t + kStages < ntile) {
             mbar_expect_tx(&full[s], kStageTx);
@@ -439,6 +481,7 @@ __global__ void __launch_bounds__(kThreads, kJerk ? FK_MINB : FK_MINB_ACC) force
                 tma_load_1d(ring64 + s * kTile, a.pk64 + jc0 + (int64_t)(t + kStages) * kTile,
                             kT64TileBytes, &full[s]);
         }
+#endif
     }
 
     // chunk partial [chunk][kNC][n_loc_pad], coalesced fp64 stores

@@ -16,11 +16,10 @@ OUT = os.path.join(ROOT, "scripts", "sweep")
 
 VARIANTS = {
     "base":      dict(),
-    "t64b4":     dict(FK_THREADS=64, FK_MINB=4),
-    "t256b1":    dict(FK_THREADS=256, FK_MINB=1),
-    "u3":        dict(FK_UNROLL=3),
-    "st3":       dict(FK_STAGES=3),
-    "st4u1":     dict(FK_STAGES=4, FK_UNROLL=1),
+    "pf":        dict(FK_PREFETCH=1),
+    "pfu1":      dict(FK_PREFETCH=1, FK_UNROLL=1),
+    "pfu4":      dict(FK_PREFETCH=1, FK_UNROLL=4),
+    "pfst3":     dict(FK_PREFETCH=1, FK_STAGES=3),
 }
 if os.environ.get("SWEEP_ONLY"):
     VARIANTS = {k: v for k, v in VARIANTS.items() if k in os.environ["SWEEP_ONLY"].split(",")}
