@@ -60,6 +60,11 @@ def _load():
     lib.oracle_hermite.restype = ctypes.c_int
     lib.oracle_leapfrog.argtypes = [i64, d, d, d, i64, p, p, p, p, ctypes.c_int]
     lib.oracle_leapfrog.restype = ctypes.c_int
+    i32 = ctypes.c_int
+    lib.oracle_block_init_levels.argtypes = [i64, d, i32, d, p, p, p, p]
+    lib.oracle_block_init_levels.restype = ctypes.c_int
+    lib.oracle_hermite_block.argtypes = [i64, d, d, d, i32, d, d, i64, p, p, p, p, p, p, i32, p, p]
+    lib.oracle_hermite_block.restype = ctypes.c_int
     lib.oracle_threads.argtypes = []
     lib.oracle_threads.restype = ctypes.c_int
     lib.oracle_set_threads.argtypes = [ctypes.c_int]
@@ -177,3 +182,50 @@ def leapfrog(m, x, v, eps2: float, dt: float, nsteps: int, G: float = 1.0, acc=N
     if rc:
         raise OracleError(f"oracle_leapfrog failed rc={rc}")
     return x, v, acc
+
+
+def block_init_levels(acc, jerk, dt_max: float, kmax: int, eta_s: float):
+    """Initial block levels k (dt = dt_max / 2^k) from eta_s |a| / |j| (R#28).
+
+    Returns (level int32 [n], criterion fp64 [n])."""
+    acc = _f64(acc)
+    n = acc.shape[1]
+    jerk = _f64(jerk, (3, n))
+    level = np.zeros(n, dtype=np.int32)
+    crit = np.zeros(n)
+    _load().oracle_block_init_levels(n, float(dt_max), int(kmax), float(eta_s), _ptr(acc),
+                                     _ptr(jerk), _ptr(level), _ptr(crit))
+    return level, crit
+
+
+def hermite_block(m, x, v, eps2: float, dt_max: float, ncycles: int, eta: float,
+                  eta_s: float = 0.01, kmax: int = 20, G: float = 1.0, acc=None, jerk=None,
+                  level=None):
+    """Advance (x, v) by ncycles * dt_max with block (individual) time steps (R#28).
+
+    If acc/jerk/level are None, forces and initial levels are evaluated first.
+    Returns (x, v, acc, jerk, level, stats, crit): stats = (block steps, sum of
+    active counts), crit = the last Aarseth criterion value of every particle.
+    """
+    m = _f64(m)
+    n = m.shape[0]
+    x = _f64(x, (3, n)).copy()
+    v = _f64(v, (3, n)).copy()
+    init = acc is None or jerk is None or level is None
+    acc = np.zeros((3, n)) if init else _f64(acc, (3, n)).copy()
+    jerk = np.zeros((3, n)) if init else _f64(jerk, (3, n)).copy()
+    level = (np.zeros(n, dtype=np.int32) if init
+             else np.ascontiguousarray(level, dtype=np.int32).copy())
+    stats = np.zeros(2, dtype=np.int64)
+    crit = np.full(n, np.nan)
+    rc = _load().oracle_hermite_block(n, float(G), float(eps2), float(dt_max), int(kmax),
+                                      float(eta), float(eta_s), int(ncycles), _ptr(m), _ptr(x),
+                                      _ptr(v), _ptr(acc), _ptr(jerk), _ptr(level),
+                                      1 if init else 0, _ptr(stats), _ptr(crit))
+    if rc == 1:
+        raise OracleError("coincident pair with eps = 0")
+    if rc == 3:
+        raise OracleError("non-finite state")
+    if rc:
+        raise OracleError(f"oracle_hermite_block failed rc={rc}")
+    return x, v, acc, jerk, level, (int(stats[0]), int(stats[1])), crit

@@ -267,3 +267,137 @@ done:
     free(jerk);
     return rc;
 }
+
+/*
+ * ---------------------------------------------------------------------------
+ * Block (individual) time steps -- SURVEY 8(f) row f4, "then block
+ * (individual) time steps": the production form of the 4th-order Hermite
+ * scheme of R#3 (reading R#28).  Every particle carries its own
+ * step dt_i = dt_max / 2^k_i (level k_i, 0 <= k_i <= kmax) and its own time
+ * t_i; times are held exactly as integer ticks of dt_max / 2^kmax.  One block
+ * step, in this order:
+ *   1. t_next = min_i (t_i + dt_i); the active set A = {i : t_i + dt_i == t_next}
+ *   2. predict every particle j to t_next with its own Taylor polynomial,
+ *      D = t_next - t_j:  xp = x + v D + a D^2/2 + j D^3/6,  vp = v + a D + j D^2/2
+ *      (the predictor of oracle_hermite with dt -> D)
+ *   3. (a1, j1) for i in A from all predicted j != i (oracle_forces)
+ *   4. correct i in A with the corrector of oracle_hermite and dt = dt_i
+ *   5. new step from the Aarseth criterion at t_next with the interpolated
+ *      derivatives a^(2)(t_next) = a2 + dt_i a3, a^(3) = a3:
+ *        dt_c = sqrt(eta (|a1| |a^(2)| + |j1|^2) / (|j1| |a^(3)| + |a^(2)|^2))
+ *      and the block rules: if dt_c < dt_i halve until dt_i <= dt_c (or
+ *      k == kmax); else if dt_c >= 2 dt_i and t_next is a multiple of 2 dt_i,
+ *      double once; otherwise keep.  t_i <- t_next, a0 <- a1, j0 <- j1.
+ * Initial levels (init != 0): the largest dt_max / 2^k <= eta_s |a| / |j|
+ * (k = 0 when j = 0).  One call advances ncycles * dt_max; every particle is
+ * synchronised at the end.  level [n] in/out, stats[0] += block steps,
+ * stats[1] += sum over block steps of |A|.  crit [n] (may be NULL) receives
+ * the last criterion value dt_c of every particle (eta_s |a|/|j| after init).
+ * Returns 0, 1 coincident pair, 2 allocation failure, 3 non-finite state,
+ * 4 invalid arguments.
+ */
+static double block_dt(double dt_max, int k) { return ldexp(dt_max, -k); }
+
+static double norm3(const double* p, int64_t n, int64_t i) {
+    return sqrt(p[0 * n + i] * p[0 * n + i] + p[1 * n + i] * p[1 * n + i] + p[2 * n + i] * p[2 * n + i]);
+}
+
+int oracle_block_init_levels(int64_t n, double dt_max, int kmax, double eta_s, const double* acc,
+                             const double* jerk, int32_t* level, double* crit) {
+    for (int64_t i = 0; i < n; ++i) {
+        const double an = norm3(acc, n, i), jn = norm3(jerk, n, i);
+        const double dts = jn > 0.0 ? eta_s * an / jn : INFINITY;
+        int k = 0;
+        while (k < kmax && block_dt(dt_max, k) > dts) ++k;
+        level[i] = k;
+        if (crit) crit[i] = dts;
+    }
+    return 0;
+}
+
+int oracle_hermite_block(int64_t n, double G, double eps2, double dt_max, int kmax, double eta,
+                         double eta_s, int64_t ncycles, const double* m, double* x, double* v,
+                         double* acc, double* jerk, int32_t* level, int init, int64_t* stats,
+                         double* crit) {
+    if (n < 1 || kmax < 0 || kmax > 50 || ncycles < 0 || !(dt_max > 0.0) || !(eta > 0.0)) return 4;
+    const size_t sz = sizeof(double) * 3 * (size_t)n;
+    double* xp = (double*)malloc(sz);
+    double* vp = (double*)malloc(sz);
+    int64_t* T = (int64_t*)malloc(sizeof(int64_t) * (size_t)n);
+    int64_t* act = (int64_t*)malloc(sizeof(int64_t) * (size_t)n);
+    double* a1 = (double*)malloc(sz);
+    double* j1 = (double*)malloc(sz);
+    int rc = 0;
+    if (!xp || !vp || !T || !act || !a1 || !j1) { rc = 2; goto done; }
+    if (init) {
+        if (oracle_forces(n, G, eps2, m, x, v, NULL, n, acc, jerk, NULL)) { rc = 1; goto done; }
+        oracle_block_init_levels(n, dt_max, kmax, eta_s, acc, jerk, level, crit);
+    }
+    const double tick = ldexp(dt_max, -kmax);
+    const int64_t T_end = ncycles << kmax;
+    for (int64_t i = 0; i < n; ++i) {
+        if (level[i] < 0 || level[i] > kmax) { rc = 4; goto done; }
+        T[i] = 0;
+    }
+    for (;;) {
+        /* 1. next block time and the active set */
+        int64_t T_next = INT64_MAX;
+        for (int64_t i = 0; i < n; ++i) {
+            const int64_t Ti = T[i] + ((int64_t)1 << (kmax - level[i]));
+            if (Ti < T_next) T_next = Ti;
+        }
+        if (T_next > T_end) break;
+        int64_t na = 0;
+        for (int64_t i = 0; i < n; ++i)
+            if (T[i] + ((int64_t)1 << (kmax - level[i])) == T_next) act[na++] = i;
+        /* 2. predict everyone to t_next */
+        for (int64_t j = 0; j < n; ++j) {
+            const double D = (double)(T_next - T[j]) * tick, D2 = D * D, D3 = D2 * D;
+            for (int c = 0; c < 3; ++c) {
+                const int64_t k = c * n + j;
+                xp[k] = x[k] + v[k] * D + acc[k] * D2 / 2.0 + jerk[k] * D3 / 6.0;
+                vp[k] = v[k] + acc[k] * D + jerk[k] * D2 / 2.0;
+            }
+        }
+        /* 3. forces on the active particles from all predicted particles */
+        if (oracle_forces(n, G, eps2, m, xp, vp, act, na, a1, j1, NULL)) { rc = 1; goto done; }
+        /* 4.-5. correct, new step */
+        for (int64_t q = 0; q < na; ++q) {
+            const int64_t i = act[q];
+            const int ki = level[i];
+            const double dt = block_dt(dt_max, ki);
+            const double dt2 = dt * dt, dt3 = dt2 * dt, dt4 = dt3 * dt, dt5 = dt4 * dt;
+            double s_a1 = 0, s_j1 = 0, s_a2 = 0, s_a3 = 0;
+            for (int c = 0; c < 3; ++c) {
+                const int64_t k = c * n + i;
+                const double A1 = a1[c * na + q], J1 = j1[c * na + q];
+                const double a2 = (-6.0 * (acc[k] - A1) - dt * (4.0 * jerk[k] + 2.0 * J1)) / dt2;
+                const double a3 = (12.0 * (acc[k] - A1) + 6.0 * dt * (jerk[k] + J1)) / dt3;
+                x[k] = xp[k] + a2 * dt4 / 24.0 + a3 * dt5 / 120.0;
+                v[k] = vp[k] + a2 * dt3 / 6.0 + a3 * dt4 / 24.0;
+                acc[k] = A1;
+                jerk[k] = J1;
+                const double a2t = a2 + dt * a3;     /* a^(2) at t_next */
+                s_a1 += A1 * A1; s_j1 += J1 * J1; s_a2 += a2t * a2t; s_a3 += a3 * a3;
+                if (!isfinite(x[k]) || !isfinite(v[k])) rc = 3;
+            }
+            const double na1 = sqrt(s_a1), nj1 = sqrt(s_j1), na2 = sqrt(s_a2), na3 = sqrt(s_a3);
+            const double den = nj1 * na3 + na2 * na2;
+            const double dtc = den > 0.0 ? sqrt(eta * (na1 * na2 + nj1 * nj1) / den) : INFINITY;
+            int kn = ki;
+            if (dtc < dt) {
+                while (kn < kmax && block_dt(dt_max, kn) > dtc) ++kn;
+            } else if (ki > 0 && dtc >= 2.0 * dt && T_next % ((int64_t)2 << (kmax - ki)) == 0) {
+                kn = ki - 1;
+            }
+            level[i] = kn;
+            T[i] = T_next;
+            if (crit) crit[i] = dtc;
+        }
+        if (rc) goto done;
+        if (stats) { stats[0] += 1; stats[1] += na; }
+    }
+done:
+    free(xp); free(vp); free(T); free(act); free(a1); free(j1);
+    return rc;
+}

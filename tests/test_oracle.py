@@ -374,3 +374,98 @@ def test_leapfrog_free_particle_and_energy():
     E0 = sum(oracle.energy(m, x, v, 0.0))
     E1 = sum(oracle.energy(m, x1, v1, 0.0))
     assert abs((E1 - E0) / E0) < 1e-5      # symplectic: bounded, O(dt^2) energy error
+
+
+# ------------------------------------------------------- block time steps (R#28)
+
+def _kep_rel_e(e, t):
+    E = t if e < 0.8 else math.pi
+    for _ in range(100):
+        E -= (E - e * math.sin(E) - t) / (1 - e * math.cos(E))
+    return np.array([math.cos(E) - e, math.sqrt(1 - e * e) * math.sin(E), 0.0])
+
+
+def test_block_reduces_to_shared_step_bitwise():
+    """With eta, eta_s -> infinity every particle stays on level 0 (dt = dt_max), and the
+    block scheme is the shared-dt Hermite scheme of R#3 operation for operation."""
+    m, x, v = inputs.make("C1")
+    xs, vs, as_, js = oracle.hermite(m, x, v, 1e-4, 1 / 1024, 4)
+    xb, vb, ab, jb, lev, st, _ = oracle.hermite_block(m, x, v, 1e-4, 1 / 1024, 4, eta=1e30,
+                                                      eta_s=1e30)
+    assert np.array_equal(xs, xb) and np.array_equal(vs, vb)
+    assert np.array_equal(as_, ab) and np.array_equal(js, jb)
+    assert lev.max() == 0 and st == (4, 4 * 1024)
+
+
+def test_block_startup_level_closed_form():
+    """Circular binary (omega = 1): |a| / |j| = 1 / omega, so eta_s |a|/|j| = eta_s and the
+    startup level is the largest 2^-k <= eta_s: k = 7 for eta_s = 0.01, dt_max = 1."""
+    m, x, v = inputs.kepler(0.0)
+    a, j = oracle.forces(m, x, v, 0.0)
+    lev, crit = oracle.block_init_levels(a, j, 1.0, 30, 0.01)
+    assert np.allclose(crit, 0.01, rtol=1e-14, atol=0)
+    assert list(lev) == [7, 7]
+    lev, _ = oracle.block_init_levels(a, j, 1.0, 5, 0.01)     # capped at kmax
+    assert list(lev) == [5, 5]
+
+
+def test_block_aarseth_criterion_circular_orbit():
+    """Aarseth criterion on a circular orbit: |a^(n)| = A omega^n, so
+    dt = sqrt(eta (2 A^2 omega^2) / (2 A^2 omega^4)) = sqrt(eta) / omega (closed form).
+    The oracle's value (from Hermite-interpolated a^(2), a^(3)) must match to O(dt^2)."""
+    m, x, v = inputs.kepler(0.0)
+    for eta in (0.01, 0.0025):
+        _, _, _, _, lev, _, crit = oracle.hermite_block(m, x, v, 0.0, 1.0, 1, eta=eta,
+                                                        eta_s=0.01, kmax=30)
+        assert np.allclose(crit, math.sqrt(eta), rtol=1e-2, atol=0), (eta, crit)
+        # the level that the criterion selects: largest 2^-k <= sqrt(eta)
+        assert list(lev) == [int(math.ceil(-math.log2(math.sqrt(eta))))] * 2
+
+
+@pytest.mark.parametrize("e", [0.5, 0.9])
+def test_block_kepler_fourth_order_in_sqrt_eta(e):
+    """Adaptive Hermite: dt ~ sqrt(eta), error ~ dt^4 ~ eta^2: eta / 4 halves every step
+    and divides the one-period error (vs the Kepler closed form) by ~16 (accept [10, 24])."""
+    errs, steps = [], []
+    for eta in (0.004, 0.001):
+        m, x, v = inputs.kepler(e)
+        xb, _, _, _, _, st, _ = oracle.hermite_block(m, x, v, 0.0, 2 * math.pi / 16, 16, eta=eta,
+                                                     eta_s=0.01, kmax=30)
+        errs.append(np.linalg.norm((xb[:, 1] - xb[:, 0]) - _kep_rel_e(e, 2 * math.pi)))
+        steps.append(st[0])
+    assert 10.0 <= errs[0] / errs[1] <= 24.0, errs
+    assert 1.8 <= steps[1] / steps[0] <= 2.2, steps
+    assert errs[1] < (3e-7 if e == 0.5 else 3e-6)
+
+
+def test_block_plummer_converges_to_small_shared_step():
+    """N = 32 Plummer with a spread of levels (particles predicted to each other's block
+    times): the block solution converges at 4th order in dt ~ sqrt(eta) to a shared-dt
+    reference at dt = 2^-14 (a wrong predictor or corrector for unsynchronised particles
+    breaks the ratio)."""
+    m, x, v = inputs.plummer(32, 11)
+    xr, _, _, _ = oracle.hermite(m, x, v, 1e-4, 2.0 ** -14, 2 ** 12)
+    errs = []
+    for eta in (0.02, 0.005):
+        xb, _, _, _, lev, _, _ = oracle.hermite_block(m, x, v, 1e-4, 1 / 16, 4, eta=eta,
+                                                      eta_s=0.01, kmax=30)
+        assert lev.max() - lev.min() >= 3        # genuinely individual steps
+        errs.append(np.max(np.abs(xb - xr)))
+    assert 10.0 <= errs[0] / errs[1] <= 24.0, errs
+    assert errs[1] < 1e-8
+
+
+def test_block_chaining_and_energy():
+    """k cycles then k more (passing acc, jerk, level) equals 2k cycles bit for bit (call
+    boundaries are multiples of dt_max); energy conserved to ~eta^2."""
+    m, x, v = inputs.plummer(256, 12)
+    kw = dict(eta=0.02, eta_s=0.01, kmax=30)
+    xa, va, aa, ja, la, sa, _ = oracle.hermite_block(m, x, v, 1e-4, 1 / 32, 3, **kw)
+    xb, vb, _, _, lb, sb, _ = oracle.hermite_block(m, xa, va, 1e-4, 1 / 32, 3, acc=aa, jerk=ja,
+                                                   level=la, **kw)
+    xc, vc, _, _, lc, sc, _ = oracle.hermite_block(m, x, v, 1e-4, 1 / 32, 6, **kw)
+    assert np.array_equal(xb, xc) and np.array_equal(vb, vc) and np.array_equal(lb, lc)
+    assert (sa[0] + sb[0], sa[1] + sb[1]) == sc
+    E0 = sum(oracle.energy(m, x, v, 1e-4))
+    E1 = sum(oracle.energy(m, xc, vc, 1e-4))
+    assert abs((E1 - E0) / E0) < 5e-8      # measured 1.3e-8
