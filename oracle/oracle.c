@@ -292,7 +292,8 @@ done:
  * (k = 0 when j = 0).  One call advances ncycles * dt_max; every particle is
  * synchronised at the end.  level [n] in/out, stats[0] += block steps,
  * stats[1] += sum over block steps of |A|.  crit [n] (may be NULL) receives
- * the last criterion value dt_c of every particle (eta_s |a|/|j| after init).
+ * the last criterion value dt_c of every particle (eta_s |a|/|j| after init);
+ * d2_out, d3_out [3][n] (may be NULL) the a^(2)(t_next), a^(3) it used.
  * Returns 0, 1 coincident pair, 2 allocation failure, 3 non-finite state,
  * 4 invalid arguments.
  */
@@ -318,7 +319,7 @@ int oracle_block_init_levels(int64_t n, double dt_max, int kmax, double eta_s, c
 int oracle_hermite_block(int64_t n, double G, double eps2, double dt_max, int kmax, double eta,
                          double eta_s, int64_t ncycles, const double* m, double* x, double* v,
                          double* acc, double* jerk, int32_t* level, int init, int64_t* stats,
-                         double* crit) {
+                         double* crit, double* d2_out, double* d3_out) {
     if (n < 1 || kmax < 0 || kmax > 50 || ncycles < 0 || !(dt_max > 0.0) || !(eta > 0.0)) return 4;
     const size_t sz = sizeof(double) * 3 * (size_t)n;
     double* xp = (double*)malloc(sz);
@@ -378,6 +379,8 @@ int oracle_hermite_block(int64_t n, double G, double eps2, double dt_max, int km
                 acc[k] = A1;
                 jerk[k] = J1;
                 const double a2t = a2 + dt * a3;     /* a^(2) at t_next */
+                if (d2_out) d2_out[k] = a2t;
+                if (d3_out) d3_out[k] = a3;
                 s_a1 += A1 * A1; s_j1 += J1 * J1; s_a2 += a2t * a2t; s_a3 += a3 * a3;
                 if (!isfinite(x[k]) || !isfinite(v[k])) rc = 3;
             }

@@ -469,3 +469,51 @@ def test_block_chaining_and_energy():
     E0 = sum(oracle.energy(m, x, v, 1e-4))
     E1 = sum(oracle.energy(m, xc, vc, 1e-4))
     assert abs((E1 - E0) / E0) < 5e-8      # measured 1.3e-8
+
+
+def _kepler_body_accel_derivs(e, t, orders):
+    """Exact d^k a/dt^k of body 1 of inputs.kepler(e) (m = 1/2 each, G = 1): body 1 feels
+    -(1/2) r / |r|^3 with r the closed-form relative orbit; 40-digit mpmath derivatives."""
+    mp.mp.dps = 40
+
+    def acc1(s, c):
+        E = mp.mpf(s)
+        for _ in range(80):
+            E -= (E - e * mp.sin(E) - s) / (1 - e * mp.cos(E))
+        r = [mp.cos(E) - e, mp.sqrt(1 - e * e) * mp.sin(E)]
+        rn = mp.sqrt(r[0] ** 2 + r[1] ** 2)
+        return -r[c] / rn ** 3 * 0.5
+    return [np.array([float(mp.diff(lambda s: acc1(s, c), t, k)) for c in range(2)])
+            for k in orders]
+
+
+def test_block_interpolated_derivatives_converge():
+    """The criterion's a^(2)(t_next) = a2 + dt a3 and a^(3) = a3 are the 2nd and 3rd
+    derivatives of the Hermite cubic through (a0, j0, a1, j1): against the exact Kepler
+    derivatives at t_next they converge as dt^2 and dt (halving dt: ratios 4 and 2).
+    Using a2 (the value at the start of the step) instead would converge only as dt."""
+    ex2, ex3 = _kepler_body_accel_derivs(0.5, 1.0, (2, 3))
+    e2, e3 = [], []
+    for eta in (1e-3, 2.5e-4):      # eta / 4 -> one level finer (dt / 2)
+        m, x, v = inputs.kepler(0.5)
+        out = oracle.hermite_block(m, x, v, 0.0, 1.0, 1, eta=eta, eta_s=0.01, kmax=30,
+                                   derivs=True)
+        d2, d3 = out[7], out[8]
+        e2.append(np.linalg.norm(d2[:2, 1] - ex2) / np.linalg.norm(ex2))
+        e3.append(np.linalg.norm(d3[:2, 1] - ex3) / np.linalg.norm(ex3))
+        assert abs(d2[2, 1]) < 1e-12 and abs(d3[2, 1]) < 1e-9      # planar orbit
+    assert 3.2 <= e2[0] / e2[1] <= 4.8, e2
+    assert 1.6 <= e3[0] / e3[1] <= 2.4, e3
+    assert e2[1] < 2e-5 and e3[1] < 1e-2
+
+
+def test_block_level_drops_several_levels_at_once():
+    """eta_s = 1 starts the circular binary at dt = dt_max = 1; after that one step the
+    Aarseth value is ~sqrt(eta) = 0.01 and the block rule halves repeatedly (not once):
+    level 7 (dt = 2^-7 <= 0.013 < 2^-6)."""
+    m, x, v = inputs.kepler(0.0)
+    _, _, _, _, lev, st, crit = oracle.hermite_block(m, x, v, 0.0, 1.0, 1, eta=1e-4, eta_s=1.0,
+                                                     kmax=30)
+    assert st == (1, 2)
+    assert 2.0 ** -7 <= crit[0] < 2.0 ** -6
+    assert list(lev) == [7, 7]
