@@ -63,8 +63,10 @@ enum nbody_status {
 };
 
 enum nbody_integrator {
-    NBODY_HERMITE4 = 0,    /* 4th-order Hermite P(EC)^1, shared dt (R#3)        */
-    NBODY_LEAPFROG_KDK = 1 /* kick-drift-kick leapfrog, accel only (NEXT f1)    */
+    NBODY_HERMITE4 = 0,       /* 4th-order Hermite P(EC)^1, shared dt (R#3)     */
+    NBODY_LEAPFROG_KDK = 1,   /* kick-drift-kick leapfrog, accel only (NEXT f1) */
+    NBODY_HERMITE4_BLOCK = 2  /* Hermite-4 with block (individual) time steps
+                                 dt_i = dt / 2^k_i (NEXT f4, R#28)    */
 };
 
 typedef struct {
@@ -100,6 +102,14 @@ typedef struct {
                              creates a non-blocking stream; pass
                              cudaStreamLegacy ((void*)1) for the legacy
                              default stream                                    */
+    /* NBODY_HERMITE4_BLOCK only (ignored otherwise); dt above is the largest
+     * step dt_max, and every particle steps with dt_max / 2^k, 0 <= k <= kmax. */
+    double eta;           /* Aarseth accuracy parameter, finite, > 0 (0.01-0.02
+                             typical): dt_c = sqrt(eta (|a||a2| + |j|^2) /
+                             (|j||a3| + |a2|^2))                               */
+    double eta_s;         /* startup parameter, finite, > 0: first level from
+                             eta_s |a| / |j|                                   */
+    int32_t kmax;         /* deepest level, 0 <= kmax <= 50 (0 -> 20)           */
 } nbody_config;
 
 /* Partition and reduction plan (pure host function, no GPU needed).
@@ -143,14 +153,31 @@ int nbody_local_range(const nbody_ctx* ctx, int64_t* i0, int64_t* i1);
  * With eps > 0 the j == i term is exactly zero.  Collective. */
 int nbody_compute_forces(nbody_ctx* ctx, double* acc, double* jerk);
 
-/* Advances the state by nsteps >= 1 shared-dt steps of the configured
+/* Advances the state by nsteps >= 1 steps of dt of the configured
  * integrator.  Hermite: evaluates a0, j0 first if not cached, then per step
  * predict (fp64) -> exchange -> force (FP32) -> correct (fp64): exactly one
  * force evaluation per step (P(EC)^1, R#3).  Leapfrog (NEXT f1): kick
  * v += a dt/2, drift x += v dt -> exchange -> acceleration-only force pass ->
  * kick v += a dt/2, one evaluation per step.  Non-blocking; a non-finite
- * state is reported by the next blocking call.  Collective. */
+ * state is reported by the next blocking call.
+ * Block time steps (NBODY_HERMITE4_BLOCK, R#28): advances nsteps * dt with
+ * individual steps dt_i = dt / 2^k_i; each block step predicts every
+ * particle to t_next = min_i(t_i + dt_i) (fp64), exchanges the packets,
+ * evaluates forces on the active set {i : t_i + dt_i == t_next} only,
+ * corrects it with its own dt_i and picks its next level from the Aarseth
+ * criterion (halve as often as needed, double at most once and only when
+ * t_next is a multiple of 2 dt_i).  Levels start from eta_s |a| / |j| at the
+ * first step after init or nbody_set_state(keep_forces = 0).  Every
+ * particle is synchronised at the end of the call.  Blocks once per block
+ * step (the active count sizes the force launch).  Collective. */
 int nbody_step(nbody_ctx* ctx, int32_t nsteps);
+
+/* Block time steps only: block steps taken and sum over them of the active
+ * count since init (either may be NULL), and the current level k_i of every
+ * local particle (level: int32 [i1 - i0], host or device, may be NULL; all
+ * zero before the first step).  Blocks.  NBODY_EINVAL for other integrators. */
+int nbody_block_stats(nbody_ctx* ctx, int64_t* block_steps, int64_t* active_sum,
+                      int32_t* level);
 
 /* Total kinetic and potential energy of the whole system (all ranks) in
  * fp64: KE = 1/2 sum m |v|^2, PE = -G sum_{i<j} m_i m_j / sqrt(r^2 + eps^2)

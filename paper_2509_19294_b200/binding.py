@@ -15,13 +15,14 @@ import numpy as np
 from . import _build
 
 NBODY_OK, NBODY_EINVAL, NBODY_ENONFINITE, NBODY_ECUDA, NBODY_ENCCL, NBODY_ENOMEM, NBODY_ESTATE = range(7)
-NBODY_HERMITE4, NBODY_LEAPFROG_KDK = 0, 1
+NBODY_HERMITE4, NBODY_LEAPFROG_KDK, NBODY_HERMITE4_BLOCK = 0, 1, 2
+INTEGRATORS = {"hermite": NBODY_HERMITE4, "leapfrog": NBODY_LEAPFROG_KDK, "block": NBODY_HERMITE4_BLOCK}
 
 EXPORTS = (
     "nbody_plan", "nbody_nccl_unique_id", "nbody_init", "nbody_local_range",
     "nbody_compute_forces", "nbody_step", "nbody_energy", "nbody_get_state",
     "nbody_set_state", "nbody_sync", "nbody_prof_enable", "nbody_prof_read",
-    "nbody_prof_launch_times",
+    "nbody_prof_launch_times", "nbody_block_stats",
     "nbody_last_error", "nbody_destroy",
 )
 
@@ -47,6 +48,9 @@ class Config(ctypes.Structure):
         ("hilo", ctypes.c_int32),
         ("nccl_id", ctypes.c_void_p),
         ("stream", ctypes.c_void_p),
+        ("eta", ctypes.c_double),
+        ("eta_s", ctypes.c_double),
+        ("kmax", ctypes.c_int32),
     ]
 
 
@@ -92,6 +96,7 @@ def lib():
         "nbody_prof_enable": ([p, i32], ctypes.c_int),
         "nbody_prof_read": ([p, Pd, P64, P64, i32], ctypes.c_int),
         "nbody_prof_launch_times": ([p, p, i64, P64], ctypes.c_int),
+        "nbody_block_stats": ([p, P64, P64, p], ctypes.c_int),
         "nbody_last_error": ([p], ctypes.c_char_p),
         "nbody_destroy": ([p], None),
     }
@@ -147,7 +152,8 @@ class NBody:
     """
 
     def __init__(self, m, x, v, eps, dt, G=1.0, integrator="hermite", rank=0, world=1,
-                 loopback=False, nccl_id=None, device=None, stream=None, jchunks=0, hilo=False):
+                 loopback=False, nccl_id=None, device=None, stream=None, jchunks=0, hilo=False,
+                 eta=0.02, eta_s=0.01, kmax=20):
         import torch
         if not torch.cuda.is_available():
             raise NBodyError(NBODY_ECUDA, "no CUDA device: libnbody has no CPU path")
@@ -163,10 +169,11 @@ class NBody:
         m, x, v = (self._prep(a) for a in (m, x, v))
         n = int(m.shape[0])
         cfg = Config(n=n, G=float(G), eps=float(eps), dt=float(dt),
-                     integrator={"hermite": NBODY_HERMITE4, "leapfrog": NBODY_LEAPFROG_KDK}[integrator],
+                     integrator=INTEGRATORS[integrator],
                      device=int(device), rank=int(rank), world=int(world),
                      loopback=1 if loopback else 0, jchunks=int(jchunks), hilo=1 if hilo else 0,
-                     nccl_id=None, stream=raw_stream)
+                     nccl_id=None, stream=raw_stream, eta=float(eta), eta_s=float(eta_s),
+                     kmax=int(kmax))
         if nccl_id is not None:
             idbuf = (ctypes.c_uint8 * 128).from_buffer_copy(nccl_id)
             self._keep.append(idbuf)
@@ -240,6 +247,14 @@ class NBody:
         out = np.zeros(n.value)
         self._c(lib().nbody_prof_launch_times(self._ctx, out.ctypes.data, n.value, ctypes.byref(n)))
         return out
+
+    def block_stats(self, levels=False):
+        """Block time steps: (block steps, sum of active counts[, levels int32 (n_loc,)])."""
+        bs, asum = ctypes.c_int64(), ctypes.c_int64()
+        lev = np.zeros(self.n_loc, dtype=np.int32) if levels else None
+        self._c(lib().nbody_block_stats(self._ctx, ctypes.byref(bs), ctypes.byref(asum),
+                                        None if lev is None else lev.ctypes.data))
+        return (bs.value, asum.value, lev) if levels else (bs.value, asum.value)
 
     def close(self):
         if getattr(self, "_ctx", None):

@@ -22,6 +22,8 @@
 //   j      = broadcast from shared memory (LDS.128 x 2 per j per thread)
 //   producer = thread 0 issues cp.async.bulk of 8 KiB tiles (the paper's
 //            `read` kernel + circular buffers, as TMA + mbarriers)
+//   block time steps: i-slot il holds local particle ilist[il] (the active
+//            set, R#28); only the i prologue and the eps = 0 report see it
 #include "internal.h"
 
 namespace nb {
@@ -192,12 +194,13 @@ __global__ void __launch_bounds__(kThreads, kJerk ? FK_MINB : FK_MINB_ACC) force
         for (int h = 0; h < 2; ++h) {
             const int il = ib + (2 * p + h) * kThreads + tid;
             if (il < a.n_loc) {
-                const JPkt pk = a.pkt[a.i_base + il];
+                const int64_t src = a.i_base + (a.ilist ? a.ilist[il] : il);   // block steps: active slot
+                const JPkt pk = a.pkt[src];
                 const float4 P = jpkt_pos(pk), V = jpkt_vel(pk);
                 q[h][0] = -P.x; q[h][1] = -P.y; q[h][2] = -P.z;
                 q[h][3] = -V.x; q[h][4] = -V.y; q[h][5] = -V.z;
                 if (kHiLo) {
-                    const float4 Lo = a.pklo[a.i_base + il];
+                    const float4 Lo = a.pklo[src];
                     q[h][6] = -Lo.x; q[h][7] = -Lo.y; q[h][8] = -Lo.z;
                 }
             } else {  // padding i: computed, never stored
@@ -229,7 +232,7 @@ __global__ void __launch_bounds__(kThreads, kJerk ? FK_MINB : FK_MINB_ACC) force
     for (int h = 0; h < kHyb; ++h) {
         const int il = ib + (2 * kPairs + h) * kThreads + tid;
         if (il < a.n_loc) {
-            const JPkt64 pk = a.pk64[a.i_base + il];
+            const JPkt64 pk = a.pk64[a.i_base + (a.ilist ? a.ilist[il] : il)];
             hx[h] = pk.p.x; hy[h] = pk.p.y; hz[h] = pk.p.z;
             hvx[h] = pk.v.x; hvy[h] = pk.v.y; hvz[h] = pk.v.z;
         } else {
@@ -369,14 +372,16 @@ __global__ void __launch_bounds__(kThreads, kJerk ? FK_MINB : FK_MINB_ACC) force
                     const int64_t jg = jc0 + (int64_t)t * kTile + jj;
                     if (s_lo == 0.f) {
                         r_lo = 0.f;
-                        const int64_t ig = a.i_base + ib + (2 * p) * kThreads + tid;
-                        if (ig != jg && ig < a.i_base + a.n_loc && jmass != 0.f)
+                        const int sl = ib + (2 * p) * kThreads + tid;
+                        const int64_t ig = a.i_base + (a.ilist && sl < a.n_loc ? a.ilist[sl] : sl);
+                        if (ig != jg && sl < a.n_loc && jmass != 0.f)
                             atomicMin(a.coincident, (unsigned long long)ig);
                     }
                     if (s_hi == 0.f) {
                         r_hi = 0.f;
-                        const int64_t ig = a.i_base + ib + (2 * p + 1) * kThreads + tid;
-                        if (ig != jg && ig < a.i_base + a.n_loc && jmass != 0.f)
+                        const int sl = ib + (2 * p + 1) * kThreads + tid;
+                        const int64_t ig = a.i_base + (a.ilist && sl < a.n_loc ? a.ilist[sl] : sl);
+                        if (ig != jg && sl < a.n_loc && jmass != 0.f)
                             atomicMin(a.coincident, (unsigned long long)ig);
                     }
                 }
@@ -421,9 +426,10 @@ __global__ void __launch_bounds__(kThreads, kJerk ? FK_MINB : FK_MINB_ACC) force
                     if (kGuard) {
                         if (s == 0.0) {
                             ri = 0.0;
-                            const int64_t ig = a.i_base + ib + (2 * kPairs + h) * kThreads + tid;
+                            const int sl = ib + (2 * kPairs + h) * kThreads + tid;
+                            const int64_t ig = a.i_base + (a.ilist && sl < a.n_loc ? a.ilist[sl] : sl);
                             const int64_t jg = jc0 + (int64_t)t * kTile + jj;
-                            if (ig != jg && ig < a.i_base + a.n_loc && Pd.w != 0.0)
+                            if (ig != jg && sl < a.n_loc && Pd.w != 0.0)
                                 atomicMin(a.coincident, (unsigned long long)ig);
                         }
                     }

@@ -9,6 +9,9 @@
 //                         packets -> the exchange buffer
 // With integrator == NBODY_LEAPFROG_KDK (NEXT f1) the same two kernels do the
 // kick-drift and the closing kick of kick-drift-kick on accelerations only.
+// Block time steps (NEXT f4, R#28) add block_* kernels: next block time,
+// active set, predictor of every particle to it, corrector + new level of
+// the active ones.
 // Integrator reading R#3: 4th-order Hermite P(EC)^1 with shared dt and the
 // Makino-Aarseth a2/a3 corrector:
 //   xp = x + v dt + a0 dt^2/2 + j0 dt^3/6,  vp = v + a0 dt + j0 dt^2/2
@@ -181,6 +184,136 @@ __global__ void validate_kernel(StateArgs a, unsigned long long* bad2) {
     }
 }
 
+
+// ---------------------------------------------------------------- block time steps
+// NBODY_HERMITE4_BLOCK (NEXT f4, R#28): individual steps
+// dt_i = dt_max / 2^k_i; times are integer ticks of dt_max / 2^kmax, so the
+// block schedule (which particles are due, commensurability for doubling)
+// is exact integer arithmetic.  Only the level choice is floating point
+// (the Aarseth criterion, fp64 here as in the oracle).
+
+__device__ __forceinline__ int64_t ticks_of(const StateArgs& a, int k) {
+    return (int64_t)1 << (a.kmax - k);
+}
+
+__device__ __forceinline__ double dt_of(const StateArgs& a, int k) { return ldexp(a.dt, -k); }
+
+__device__ __forceinline__ double norm3(const double* p, int64_t stride, int i) {
+    const double x = p[i], y = p[stride + i], z = p[2 * stride + i];
+    return sqrt(x * x + y * y + z * z);
+}
+
+// startup level: largest dt_max / 2^k <= eta_s |a| / |j| (k = 0 when j = 0)
+__global__ void block_init_levels_kernel(StateArgs a) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < a.n_loc; i += gridDim.x * blockDim.x) {
+        const double an = norm3(a.a0, a.n_loc_pad, i), jn = norm3(a.j0, a.n_loc_pad, i);
+        const double dts = jn > 0.0 ? a.eta_s * an / jn : INFINITY;
+        int k = 0;
+        while (k < a.kmax && dt_of(a, k) > dts) ++k;
+        a.lev[i] = k;
+        a.T[i] = 0;
+    }
+}
+
+__global__ void block_reset_time_kernel(StateArgs a) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < a.n_loc; i += gridDim.x * blockDim.x)
+        a.T[i] = 0;
+}
+
+// t_next = min_i (t_i + dt_i): exact integer minimum, so order-independent;
+// one atomic per warp after a shuffle reduction
+__global__ void block_tnext_kernel(StateArgs a) {
+    unsigned long long best = ~0ull;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < a.n_loc; i += gridDim.x * blockDim.x) {
+        const unsigned long long t = (unsigned long long)(a.T[i] + ticks_of(a, a.lev[i]));
+        best = t < best ? t : best;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long u = __shfl_xor_sync(0xffffffffu, best, o);
+        best = u < best ? u : best;
+    }
+    if ((threadIdx.x & 31) == 0 && best != ~0ull) atomicMin(a.tnext, best);
+}
+
+// active set {i : t_i + dt_i == t_next}; slot order is irrelevant to the
+// results (every slot's force is the same j-loop), so an atomic append suffices
+__global__ void block_select_kernel(StateArgs a) {
+    const unsigned long long tn = *a.tnext;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < a.n_loc; i += gridDim.x * blockDim.x) {
+        if ((unsigned long long)(a.T[i] + ticks_of(a, a.lev[i])) == tn) {
+            const int slot = atomicAdd(a.nact, 1);
+            a.ilist[slot] = i;
+        }
+    }
+}
+
+// every local particle predicted to t_next with its own polynomial (the
+// predictor of predict() with dt -> D = t_next - t_i), packed for the exchange
+__global__ void block_predict_pack_kernel(StateArgs a) {
+    const unsigned long long tn = *a.tnext;
+    const double tick = ldexp(a.dt, -a.kmax);
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < a.n_loc; i += gridDim.x * blockDim.x) {
+        const double D = (double)(int64_t)(tn - (unsigned long long)a.T[i]) * tick;
+        const double D2 = D * D, D3 = D2 * D;
+        double xp[3], vp[3];
+        bool ok = true;
+        for (int c = 0; c < 3; ++c) {
+            const int64_t o = c * a.n_loc_pad + i;
+            const double x = a.x[o], v = a.v[o], ac = a.a0[o], jk = a.j0[o];
+            xp[c] = x + v * D + ac * D2 / 2.0 + jk * D3 / 6.0;
+            vp[c] = v + ac * D + jk * D2 / 2.0;
+            a.xp[o] = xp[c];
+            a.vp[o] = vp[c];
+            ok = ok && isfinite(xp[c]) && isfinite(vp[c]);
+        }
+        if (!ok) flag_bad(a.bad, a.i_base + i);
+        store_packet(a, a.i_base + i, xp, vp, a.G * a.m[i]);
+    }
+}
+
+// fold the active slots' chunk partials, Hermite corrector with the particle's
+// own dt_i (R#3 form), Aarseth criterion from a1, j1 and the interpolated
+// a^(2)(t_next) = a2 + dt a3, a^(3) = a3, block rules for the next level
+__global__ void block_correct_kernel(StateArgs a, int32_t n_act) {
+    const unsigned long long tn = *a.tnext;
+    for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n_act; q += gridDim.x * blockDim.x) {
+        const int i = a.ilist[q];
+        const int k = a.lev[i];
+        const double dt = dt_of(a, k);
+        const double dt2 = dt * dt, dt3 = dt2 * dt, dt4 = dt3 * dt, dt5 = dt4 * dt;
+        double s_a1 = 0, s_j1 = 0, s_a2 = 0, s_a3 = 0;
+        bool ok = true;
+        for (int c = 0; c < 3; ++c) {
+            const int64_t o = c * a.n_loc_pad + i;
+            const double a1 = fold(a, c, q), j1 = fold(a, 3 + c, q);
+            const double a0 = a.a0[o], j0 = a.j0[o];
+            const double a2 = (-6.0 * (a0 - a1) - dt * (4.0 * j0 + 2.0 * j1)) / dt2;
+            const double a3 = (12.0 * (a0 - a1) + 6.0 * dt * (j0 + j1)) / dt3;
+            const double x = a.xp[o] + a2 * dt4 / 24.0 + a3 * dt5 / 120.0;
+            const double v = a.vp[o] + a2 * dt3 / 6.0 + a3 * dt4 / 24.0;
+            a.x[o] = x;
+            a.v[o] = v;
+            a.a0[o] = a1;
+            a.j0[o] = j1;
+            const double a2t = a2 + dt * a3;
+            s_a1 += a1 * a1; s_j1 += j1 * j1; s_a2 += a2t * a2t; s_a3 += a3 * a3;
+            ok = ok && isfinite(x) && isfinite(v) && isfinite(a1) && isfinite(j1);
+        }
+        if (!ok) flag_bad(a.bad, a.i_base + i);
+        const double na1 = sqrt(s_a1), nj1 = sqrt(s_j1), na2 = sqrt(s_a2), na3 = sqrt(s_a3);
+        const double den = nj1 * na3 + na2 * na2;
+        const double dtc = den > 0.0 ? sqrt(a.eta * (na1 * na2 + nj1 * nj1) / den) : INFINITY;
+        int kn = k;
+        if (dtc < dt) {
+            while (kn < a.kmax && dt_of(a, kn) > dtc) ++kn;
+        } else if (k > 0 && dtc >= 2.0 * dt && tn % (2ull * (unsigned long long)ticks_of(a, k)) == 0) {
+            kn = k - 1;
+        }
+        a.lev[i] = kn;
+        a.T[i] = (int64_t)tn;
+    }
+}
+
 unsigned grid_for(int64_t n) {
     int64_t g = (n + kBlock - 1) / kBlock;
     if (g > 148 * 16) g = 148 * 16;
@@ -212,6 +345,36 @@ cudaError_t launch_fold_forces(const StateArgs& a, cudaStream_t s) {
 cudaError_t launch_correct_predict_pack(const StateArgs& a, cudaStream_t s) {
     if (a.n_loc <= 0) return cudaSuccess;
     correct_predict_pack_kernel<<<grid_for(a.n_loc), kBlock, 0, s>>>(a);
+    return cudaGetLastError();
+}
+cudaError_t launch_block_init_levels(const StateArgs& a, cudaStream_t s) {
+    if (a.n_loc <= 0) return cudaSuccess;
+    block_init_levels_kernel<<<grid_for(a.n_loc), kBlock, 0, s>>>(a);
+    return cudaGetLastError();
+}
+cudaError_t launch_block_reset_time(const StateArgs& a, cudaStream_t s) {
+    if (a.n_loc <= 0) return cudaSuccess;
+    block_reset_time_kernel<<<grid_for(a.n_loc), kBlock, 0, s>>>(a);
+    return cudaGetLastError();
+}
+cudaError_t launch_block_tnext(const StateArgs& a, cudaStream_t s) {
+    if (a.n_loc <= 0) return cudaSuccess;
+    block_tnext_kernel<<<grid_for(a.n_loc), kBlock, 0, s>>>(a);
+    return cudaGetLastError();
+}
+cudaError_t launch_block_select(const StateArgs& a, cudaStream_t s) {
+    if (a.n_loc <= 0) return cudaSuccess;
+    block_select_kernel<<<grid_for(a.n_loc), kBlock, 0, s>>>(a);
+    return cudaGetLastError();
+}
+cudaError_t launch_block_predict_pack(const StateArgs& a, cudaStream_t s) {
+    if (a.n_loc <= 0) return cudaSuccess;
+    block_predict_pack_kernel<<<grid_for(a.n_loc), kBlock, 0, s>>>(a);
+    return cudaGetLastError();
+}
+cudaError_t launch_block_correct(const StateArgs& a, int32_t n_act, cudaStream_t s) {
+    if (n_act <= 0) return cudaSuccess;
+    block_correct_kernel<<<grid_for(n_act), kBlock, 0, s>>>(a, n_act);
     return cudaGetLastError();
 }
 cudaError_t launch_fill_padding(JPkt* pkt, float4* pklo, JPkt64* pk64, int64_t from, int64_t to,

@@ -74,6 +74,8 @@ struct ForceArgs {
     float eps2;          // fp32(eps^2)
     double* partial;     // [n_chunks][ncomp][n_loc_pad] (acc x,y,z [, jerk x,y,z])
     unsigned long long* coincident;  // eps == 0 only: min global i of a coincident pair
+    const int32_t* ilist;  // block steps: local index of the particle in i-slot il, or nullptr
+                           // (slot il is particle il); partial rows are indexed by slot
 };
 
 // Launches the force pass for chunks c_first .. c_first + c_count - 1 (mod
@@ -102,6 +104,14 @@ struct StateArgs {
     float4* pklo;        // hi/lo position tails (nullptr unless hilo)
     JPkt64* pk64;        // fp64 packets (nullptr unless force_hyb() > 0)
     unsigned long long* bad;  // min global index of a non-finite particle
+    // block time steps (NBODY_HERMITE4_BLOCK, R#28); dt above is dt_max
+    int64_t* T;          // [n_loc] particle time in ticks of dt_max / 2^kmax
+    int32_t* lev;        // [n_loc] level k: dt_i = dt_max / 2^k
+    int32_t* ilist;      // [n_loc] active particles (local indices), slot order
+    int32_t* nact;       // active count (device counter)
+    unsigned long long* tnext;  // next block time in ticks (device, shared by shards)
+    int32_t kmax;
+    double eta, eta_s;
 };
 cudaError_t launch_pack_state(const StateArgs& a, cudaStream_t s);     // x, v -> pkt
 cudaError_t launch_predict_pack(const StateArgs& a, cudaStream_t s);   // x,v,a0,j0 -> xp,vp,pkt
@@ -119,5 +129,14 @@ cudaError_t launch_energy(const double4* eall, int64_t n, int64_t i_base,
                           const double* m, double eps2, double* block_sums,
                           int nblocks_max, double* out2, cudaStream_t s);
 int energy_blocks(int32_t n_loc);
+
+// block time steps (hermite.cu, R#28)
+cudaError_t launch_block_init_levels(const StateArgs& a, cudaStream_t s);  // lev from eta_s, T = 0
+cudaError_t launch_block_reset_time(const StateArgs& a, cudaStream_t s);   // T = 0 (call start)
+cudaError_t launch_block_tnext(const StateArgs& a, cudaStream_t s);        // atomicMin(tnext, T + dt)
+cudaError_t launch_block_select(const StateArgs& a, cudaStream_t s);       // ilist, nact
+cudaError_t launch_block_predict_pack(const StateArgs& a, cudaStream_t s); // all -> t_next
+// correct the n_act active particles (n_act read on the host), new levels, T = t_next
+cudaError_t launch_block_correct(const StateArgs& a, int32_t n_act, cudaStream_t s);
 
 }  // namespace nb

@@ -46,6 +46,8 @@ struct NcclApi {
     ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;
     ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
                               cudaStream_t) = nullptr;
+    ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                              cudaStream_t) = nullptr;
     const char* (*GetErrorString)(ncclResult_t) = nullptr;
 };
 
@@ -70,6 +72,7 @@ NcclApi& nccl() {
     NB_SYM(CommDestroy, "ncclCommDestroy");
     NB_SYM(CommGetAsyncError, "ncclCommGetAsyncError");
     NB_SYM(AllGather, "ncclAllGather");
+    NB_SYM(AllReduce, "ncclAllReduce");
     NB_SYM(GetErrorString, "ncclGetErrorString");
 #undef NB_SYM
     api.ok = true;
@@ -109,6 +112,9 @@ struct Shard {
     double *m = nullptr, *x = nullptr, *v = nullptr, *a0 = nullptr, *j0 = nullptr;
     double *xp = nullptr, *vp = nullptr, *partial = nullptr;
     int32_t c_lo = 0, c_hi = 0;  // local chunks [c_lo, c_hi)
+    int64_t* T = nullptr;        // block time steps: particle times (ticks), levels,
+    int32_t* lev = nullptr;      // active list (R#28)
+    int32_t* ilist = nullptr;
 };
 
 bool is_device_ptr(const void* p) {
@@ -138,6 +144,13 @@ struct nbody_ctx {
     int eblk_cap = 0;
     double* eout = nullptr;  // [nshards][2]
     unsigned long long* flags = nullptr;  // [0] non-finite, [1] coincident, [2..3] validate
+    // block time steps (R#28): t_next (ticks, shared by all shards), per-shard
+    // active counts, pinned read-back of both, run statistics
+    unsigned long long* tnext = nullptr;
+    int32_t* nact = nullptr;
+    void* hbuf = nullptr;
+    bool levels_ok = false;
+    int64_t block_steps = 0, active_sum = 0;
     cudaStream_t stream = nullptr, comm_stream = nullptr;
     bool own_stream = false;
     cudaEvent_t ev_packed = nullptr, ev_gathered = nullptr;
@@ -193,7 +206,8 @@ int fail(nbody_ctx* c, int code, const char* fmt, ...) {
         CK(ctx, cudaSetDevice((ctx)->cfg.device));                                          \
     } while (0)
 
-int ncomp(const nbody_ctx* c) { return c->cfg.integrator == NBODY_HERMITE4 ? 6 : 3; }
+int ncomp(const nbody_ctx* c) { return c->cfg.integrator == NBODY_LEAPFROG_KDK ? 3 : 6; }
+bool is_block(const nbody_ctx* c) { return c->cfg.integrator == NBODY_HERMITE4_BLOCK; }
 
 nb::StateArgs state_args(nbody_ctx* c, Shard& s) {
     nb::StateArgs a;
@@ -208,24 +222,37 @@ nb::StateArgs state_args(nbody_ctx* c, Shard& s) {
     a.partial = s.partial;
     a.n_chunks = (int32_t)s.plan.n_chunks;
     a.ncomp = ncomp(c);
-    a.integrator = c->cfg.integrator;
+    a.integrator = c->cfg.integrator == NBODY_LEAPFROG_KDK ? 1 : 0;   // predictor/corrector family
     a.pkt = c->pkt;
     a.pklo = c->pklo;
     a.pk64 = c->pk64;
     a.bad = c->flags;
+    a.T = s.T;
+    a.lev = s.lev;
+    a.ilist = s.ilist;
+    a.nact = c->nact ? c->nact + (&s - c->sh.data()) : nullptr;
+    a.tnext = c->tnext;
+    a.kmax = c->cfg.kmax;
+    a.eta = c->cfg.eta;
+    a.eta_s = c->cfg.eta_s;
     return a;
 }
 
 bool use_nccl(const nbody_ctx* c) { return c->comm != nullptr; }
 
-int launch_force_range(nbody_ctx* c, Shard& s, int32_t c_first, int32_t c_count) {
-    if (c_count <= 0 || s.n_loc <= 0) return NBODY_OK;
+// force pass over chunks [c_first, c_first + c_count) for the shard's local
+// particles, or (block steps) for the n_i active particles listed in ilist
+int launch_force_range(nbody_ctx* c, Shard& s, int32_t c_first, int32_t c_count, int32_t n_i = -1,
+                       const int32_t* ilist = nullptr) {
+    if (n_i < 0) n_i = s.n_loc;
+    if (c_count <= 0 || n_i <= 0) return NBODY_OK;
     nb::ForceArgs f;
     f.pkt = c->pkt;
     f.pklo = c->pklo;
     f.pk64 = c->pk64;
     f.i_base = s.plan.i0;
-    f.n_loc = s.n_loc;
+    f.n_loc = n_i;
+    f.ilist = ilist;
     f.n_loc_pad = s.n_loc_pad;
     f.chunk = (int32_t)s.plan.chunk;
     f.n_chunks = (int32_t)s.plan.n_chunks;
@@ -248,7 +275,7 @@ int launch_force_range(nbody_ctx* c, Shard& s, int32_t c_first, int32_t c_count)
         c->prof_used += 2;
         CK(c, cudaEventRecord(e0, c->stream));
     }
-    CK(c, nb::launch_force(f, c->eps2f == 0.f, c->cfg.integrator == NBODY_HERMITE4, c->stream));
+    CK(c, nb::launch_force(f, c->eps2f == 0.f, ncomp(c) == 6, c->stream));
     if (e1) CK(c, cudaEventRecord(e1, c->stream));
     c->n_force++;
     c->n_kernels++;
@@ -258,28 +285,33 @@ int launch_force_range(nbody_ctx* c, Shard& s, int32_t c_first, int32_t c_count)
 // exchange the packets written by every shard's pack kernel, then run the
 // force pass of every shard: local chunks first (overlapping the
 // all-gather), remote chunks after it.
+// in-place all-gather of every rank's packet slice (and hi/lo tails, fp64
+// packets when present) on stream st
+int gather_packets(nbody_ctx* c, cudaStream_t st) {
+    Shard& s = c->sh[0];
+    float* base = reinterpret_cast<float*>(c->pkt);
+    const size_t cnt = (size_t)s.plan.slot * (sizeof(JPkt) / sizeof(float));
+    CKNCCL(c, nccl().AllGather(base + (size_t)c->cfg.rank * cnt, base, cnt, ncclFloat32, c->comm, st));
+    if (c->pklo) {
+        float* lo = reinterpret_cast<float*>(c->pklo);
+        const size_t cl = (size_t)s.plan.slot * 4;
+        CKNCCL(c, nccl().AllGather(lo + (size_t)c->cfg.rank * cl, lo, cl, ncclFloat32, c->comm, st));
+    }
+    if (c->pk64) {
+        double* d64 = reinterpret_cast<double*>(c->pk64);
+        const size_t c8 = (size_t)s.plan.slot * 8;
+        CKNCCL(c, nccl().AllGather(d64 + (size_t)c->cfg.rank * c8, d64, c8, ncclFloat64, c->comm, st));
+    }
+    return NBODY_OK;
+}
+
 int exchange_and_force(nbody_ctx* c) {
     int rc;
     if (use_nccl(c)) {
         Shard& s = c->sh[0];
         CK(c, cudaEventRecord(c->ev_packed, c->stream));
         CK(c, cudaStreamWaitEvent(c->comm_stream, c->ev_packed, 0));
-        float* base = reinterpret_cast<float*>(c->pkt);
-        const size_t cnt = (size_t)s.plan.slot * (sizeof(JPkt) / sizeof(float));
-        CKNCCL(c, nccl().AllGather(base + (size_t)c->cfg.rank * cnt, base, cnt, ncclFloat32, c->comm,
-                                   c->comm_stream));
-        if (c->pklo) {
-            float* lo = reinterpret_cast<float*>(c->pklo);
-            const size_t cl = (size_t)s.plan.slot * 4;
-            CKNCCL(c, nccl().AllGather(lo + (size_t)c->cfg.rank * cl, lo, cl, ncclFloat32, c->comm,
-                                       c->comm_stream));
-        }
-        if (c->pk64) {
-            double* d64 = reinterpret_cast<double*>(c->pk64);
-            const size_t c8 = (size_t)s.plan.slot * 8;
-            CKNCCL(c, nccl().AllGather(d64 + (size_t)c->cfg.rank * c8, d64, c8, ncclFloat64, c->comm,
-                                       c->comm_stream));
-        }
+        if ((rc = gather_packets(c, c->comm_stream))) return rc;
         CK(c, cudaEventRecord(c->ev_gathered, c->comm_stream));
         // Overlap: while the all-gather runs, compute a whole number of waves of
         // local-chunk work items (i-block x chunk) -- a partial wave here would
@@ -369,7 +401,11 @@ void free_ctx(nbody_ctx* c) {
     for (auto& s : c->sh) {
         cudaFree(s.m); cudaFree(s.x); cudaFree(s.v); cudaFree(s.a0); cudaFree(s.j0);
         cudaFree(s.xp); cudaFree(s.vp); cudaFree(s.partial);
+        cudaFree(s.T); cudaFree(s.lev); cudaFree(s.ilist);
     }
+    cudaFree(c->tnext);
+    cudaFree(c->nact);
+    if (c->hbuf) cudaFreeHost(c->hbuf);
     cudaFree(c->pkt);
     cudaFree(c->pklo);
     cudaFree(c->pk64);
@@ -404,12 +440,21 @@ int init_impl(const nbody_config* cfg, const double* m, const double* x, const d
     if (!(std::isfinite(k.G) && k.G > 0)) return fail(c, NBODY_EINVAL, "G must be finite and > 0");
     if (!(std::isfinite(k.eps) && k.eps >= 0)) return fail(c, NBODY_EINVAL, "eps must be finite and >= 0");
     if (!(std::isfinite(k.dt) && k.dt > 0)) return fail(c, NBODY_EINVAL, "dt must be finite and > 0");
-    if (k.integrator != NBODY_HERMITE4 && k.integrator != NBODY_LEAPFROG_KDK)
+    if (k.integrator != NBODY_HERMITE4 && k.integrator != NBODY_LEAPFROG_KDK &&
+        k.integrator != NBODY_HERMITE4_BLOCK)
         return fail(c, NBODY_EINVAL, "integrator %d not supported", k.integrator);
+    if (k.integrator == NBODY_HERMITE4_BLOCK) {
+        if (!(std::isfinite(k.eta) && k.eta > 0))
+            return fail(c, NBODY_EINVAL, "eta must be finite and > 0 for block time steps");
+        if (!(std::isfinite(k.eta_s) && k.eta_s > 0))
+            return fail(c, NBODY_EINVAL, "eta_s must be finite and > 0 for block time steps");
+        if (k.kmax < 0 || k.kmax > 50) return fail(c, NBODY_EINVAL, "kmax must be in [0, 50]");
+    }
     if (!m || !x || !v) return fail(c, NBODY_EINVAL, "m, x and v must be non-NULL");
     if (k.world > 1 && !k.loopback && !k.nccl_id)
         return fail(c, NBODY_EINVAL, "world > 1 needs nccl_id (or loopback)");
     c->cfg = k;
+    if (k.integrator == NBODY_HERMITE4_BLOCK && k.kmax == 0) c->cfg.kmax = 20;
     c->n = k.n;
     const char* ng = getenv("NBODY_NO_GRAPH");
     c->use_graph = !(ng && *ng && *ng != '0');
@@ -441,6 +486,10 @@ int init_impl(const nbody_config* cfg, const double* m, const double* x, const d
     if (k.hilo && (rc = dalloc(c, &c->pklo, (size_t)c->L))) return rc;
     if (nb::force_hyb() > 0 && (rc = dalloc(c, &c->pk64, (size_t)c->L))) return rc;
     if ((rc = dalloc(c, &c->flags, 4))) return rc;
+    if (is_block(c)) {
+        if ((rc = dalloc(c, &c->tnext, 1)) || (rc = dalloc(c, &c->nact, (size_t)c->nshards))) return rc;
+        CK(c, cudaMallocHost(&c->hbuf, 8 + 4 * (size_t)c->nshards));
+    }
     CK(c, cudaMemsetAsync(c->flags, 0xff, 4 * sizeof(unsigned long long), c->stream));
     CK(c, nb::launch_fill_padding(c->pkt, c->pklo, c->pk64, 0, c->L, c->eps2f, c->stream));
     c->n_kernels++;
@@ -455,6 +504,13 @@ int init_impl(const nbody_config* cfg, const double* m, const double* x, const d
             (rc = dalloc(c, &s.j0, v3)) || (rc = dalloc(c, &s.xp, v3)) || (rc = dalloc(c, &s.vp, v3)))
             return rc;
         if ((rc = dalloc(c, &s.partial, (size_t)s.plan.n_chunks * ncomp(c) * s.n_loc_pad))) return rc;
+        if (is_block(c)) {
+            if ((rc = dalloc(c, &s.T, (size_t)s.n_loc_pad)) || (rc = dalloc(c, &s.lev, (size_t)s.n_loc_pad)) ||
+                (rc = dalloc(c, &s.ilist, (size_t)s.n_loc_pad)))
+                return rc;
+            CK(c, cudaMemsetAsync(s.T, 0, (size_t)s.n_loc_pad * sizeof(int64_t), c->stream));
+            CK(c, cudaMemsetAsync(s.lev, 0, (size_t)s.n_loc_pad * sizeof(int32_t), c->stream));
+        }
         // local chunks: those inside [i0, i0 + slot) of this rank's exchange slice
         const int64_t lo = s.plan.i0 == s.plan.i1 ? 0 : s.plan.i0;
         const int64_t hi = s.plan.i0 == s.plan.i1 ? 0 : s.plan.i0 + s.plan.slot;
@@ -577,10 +633,73 @@ int one_step(nbody_ctx* c) {
 }
 }  // namespace
 
+namespace {
+// Block time steps (R#28): nsteps * dt_max of individual Hermite steps.  Per
+// block step: t_next = min(t_i + dt_i) (device reduction, NCCL min over ranks),
+// active list, predict + pack everything, exchange, force pass on the active
+// slots only, correct + new level.  t_next and the active counts come back to
+// the host each block step: they end the loop and size the force grid.
+int block_run(nbody_ctx* c, int32_t nsteps) {
+    int rc;
+    const int kmax = c->cfg.kmax;
+    if ((int64_t)nsteps > (INT64_MAX >> (kmax + 1)))
+        return fail(c, NBODY_EINVAL, "nsteps * 2^kmax overflows the block clock");
+    if ((rc = ensure_forces(c))) return rc;
+    for (auto& s : c->sh) {
+        if (c->levels_ok)
+            CK(c, nb::launch_block_reset_time(state_args(c, s), c->stream));   // all synchronised
+        else
+            CK(c, nb::launch_block_init_levels(state_args(c, s), c->stream));
+        c->n_kernels++;
+    }
+    c->levels_ok = true;
+    const unsigned long long T_end = (unsigned long long)nsteps << kmax;
+    unsigned long long* h_tnext = reinterpret_cast<unsigned long long*>(c->hbuf);
+    int32_t* h_nact = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(c->hbuf) + 8);
+    for (;;) {
+        CK(c, cudaMemsetAsync(c->tnext, 0xff, sizeof(unsigned long long), c->stream));
+        CK(c, cudaMemsetAsync(c->nact, 0, sizeof(int32_t) * c->nshards, c->stream));
+        for (auto& s : c->sh) {
+            CK(c, nb::launch_block_tnext(state_args(c, s), c->stream));
+            c->n_kernels++;
+        }
+        if (use_nccl(c))
+            CKNCCL(c, nccl().AllReduce(c->tnext, c->tnext, 1, ncclUint64, ncclMin, c->comm, c->stream));
+        for (auto& s : c->sh) {
+            CK(c, nb::launch_block_select(state_args(c, s), c->stream));
+            c->n_kernels++;
+        }
+        CK(c, cudaMemcpyAsync(c->hbuf, c->tnext, 8, cudaMemcpyDeviceToHost, c->stream));
+        CK(c, cudaMemcpyAsync(h_nact, c->nact, 4 * (size_t)c->nshards, cudaMemcpyDeviceToHost, c->stream));
+        CK(c, cudaStreamSynchronize(c->stream));
+        if (*h_tnext > T_end) break;
+        for (auto& s : c->sh) {
+            CK(c, nb::launch_block_predict_pack(state_args(c, s), c->stream));
+            c->n_kernels++;
+        }
+        if (use_nccl(c) && (rc = gather_packets(c, c->stream))) return rc;
+        int64_t na = 0;
+        for (int q = 0; q < c->nshards; ++q) {
+            Shard& s = c->sh[q];
+            if ((rc = launch_force_range(c, s, 0, (int32_t)s.plan.n_chunks, h_nact[q], s.ilist))) return rc;
+            na += h_nact[q];
+        }
+        for (int q = 0; q < c->nshards; ++q) {
+            CK(c, nb::launch_block_correct(state_args(c, c->sh[q]), h_nact[q], c->stream));
+            c->n_kernels++;
+        }
+        c->block_steps++;
+        c->active_sum += na;
+    }
+    return NBODY_OK;
+}
+}  // namespace
+
 int nbody_step(nbody_ctx* c, int32_t nsteps) {
     GUARD(c);
     if (nsteps < 1) return fail(c, NBODY_EINVAL, "nsteps must be >= 1");
     int rc;
+    if (is_block(c)) return block_run(c, nsteps);
     if ((rc = ensure_forces(c))) return rc;
     if (!c->predicted) {
         for (auto& s : c->sh) {
@@ -699,8 +818,27 @@ int nbody_set_state(nbody_ctx* c, const double* x, const double* v, int32_t keep
         c->predicted = false;
         return fail(c, NBODY_EINVAL, "position or velocity of particle %llu is not finite", bad[1]);
     }
-    if (!keep_forces) c->have_a0 = false;
+    if (!keep_forces) {
+        c->have_a0 = false;
+        c->levels_ok = false;   // block steps: levels restart from eta_s
+    }
     c->predicted = false;
+    return NBODY_OK;
+}
+
+int nbody_block_stats(nbody_ctx* c, int64_t* block_steps, int64_t* active_sum, int32_t* level) {
+    GUARD(c);
+    if (!is_block(c)) return fail(c, NBODY_EINVAL, "nbody_block_stats needs NBODY_HERMITE4_BLOCK");
+    if (level) {
+        const int64_t k0 = c->sh.front().plan.i0;
+        for (auto& s : c->sh)
+            if (s.n_loc > 0)
+                CK(c, cudaMemcpyAsync(level + (s.plan.i0 - k0), s.lev, 4 * (size_t)s.n_loc, cudaMemcpyDefault,
+                                      c->stream));
+    }
+    CK(c, cudaStreamSynchronize(c->stream));
+    if (block_steps) *block_steps = c->block_steps;
+    if (active_sum) *active_sum = c->active_sum;
     return NBODY_OK;
 }
 

@@ -1,0 +1,173 @@
+"""GPU parity of block (individual) time steps, NBODY_HERMITE4_BLOCK (SURVEY 8(f) row f4,
+DESIGN.md R#28), against the oracle's oracle_hermite_block.
+
+The level of a particle is an integer decided by floating point (the Aarseth criterion on
+fp32-force derivatives on the GPU, fp64 in the oracle).  Where the criterion sits within
+round-off of a power-of-two boundary both levels are valid, so level agreement is checked
+on the particles whose oracle criterion is clear of a boundary, and trajectories / energy
+are compared with tolerances that hold whichever valid level was taken.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_2509_19294_b200 import binding, inputs
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+
+def eps2_of(eps):
+    return float(np.float32(eps * eps))
+
+
+def run_block(m, x, v, eps, dt_max, ncycles, eta=0.02, eta_s=0.01, kmax=20, **kw):
+    with binding.NBody(m, x, v, eps=eps, dt=dt_max, integrator="block", eta=eta, eta_s=eta_s,
+                       kmax=kmax, **kw) as s:
+        s.step(ncycles)
+        xs, vs = s.state()
+        steps, active, lev = s.block_stats(levels=True)
+        s.sync()
+        return xs.cpu().numpy(), vs.cpu().numpy(), lev, (steps, active)
+
+
+def test_block_reduces_to_shared_step_bitwise():
+    """eta, eta_s -> infinity: every particle stays at dt_max and the block path is the
+    shared-dt Hermite path operation for operation (predictor with D = dt_max, the same
+    corrector), so the states are bit-identical."""
+    c = inputs.CONFIGS["C1"]
+    m, x, v = inputs.make("C1")
+    xb, vb, lev, st = run_block(m, x, v, c.eps, c.dt, 4, eta=1e30, eta_s=1e30)
+    with binding.NBody(m, x, v, eps=c.eps, dt=c.dt) as s:
+        s.step(4)
+        xs, vs = (t.cpu().numpy() for t in s.state())
+    assert np.array_equal(xb, xs) and np.array_equal(vb, vs)
+    assert st == (4, 4 * c.n) and not lev.any()
+
+
+def _levels_agree(lev_gpu, lev_orc, crit_orc, dt_max, margin=1e-3):
+    """Fraction of particles with equal levels among those whose oracle criterion is clear
+    of every power-of-two boundary, and whether all disagreements are adjacent levels."""
+    l2 = np.log2(dt_max / crit_orc)
+    clear = np.abs(l2 - np.round(l2)) > margin / math.log(2)
+    same = lev_gpu == lev_orc
+    return float(np.mean(same[clear])), bool(np.all(np.abs(lev_gpu - lev_orc) <= 1)), int(clear.sum())
+
+
+def test_block_trajectory_levels_and_steps_vs_oracle():
+    """C1 Plummer (N = 1024, eps = 1e-2), dt_max = 1/64, eta = 0.02, 4 cycles: final state
+    within 1e-8 (x) / 5e-7 (v) of the oracle (measured 7e-10 / 4e-8), levels agree wherever
+    the oracle's criterion is clear of a boundary, block-step and force-evaluation counts
+    within 5 %."""
+    c = inputs.CONFIGS["C1"]
+    m, x, v = inputs.make("C1")
+    dt_max, ncyc = 1 / 64, 4
+    xg, vg, lg, sg = run_block(m, x, v, c.eps, dt_max, ncyc)
+    xo, vo, _, _, lo, so, co = oracle.hermite_block(m, x, v, eps2_of(c.eps), dt_max, ncyc,
+                                                    eta=0.02, eta_s=0.01, kmax=20)
+    assert lo.max() - lo.min() >= 3                       # genuinely individual steps
+    frac, adjacent, nclear = _levels_agree(lg, lo, co, dt_max)
+    assert nclear > 0.9 * c.n and frac >= 0.99 and adjacent, (frac, adjacent, nclear)
+    assert abs(sg[0] - so[0]) <= 0.05 * so[0] and abs(sg[1] - so[1]) <= 0.05 * so[1], (sg, so)
+    assert np.max(np.abs(xg - xo)) <= 1e-8, np.max(np.abs(xg - xo))
+    assert np.max(np.abs(vg - vo)) <= 5e-7, np.max(np.abs(vg - vo))
+
+
+def test_block_hilo_schedule_matches_oracle_c2():
+    """C2 (N = 16384, eps = 1e-3), dt_max = 1/128, one cycle with hi/lo positions (R#27):
+    mid-run states are off the fp32 grid, and the Aarseth criterion differences a0 - a1 over
+    dt^2 and dt^3, so plain fp32 positions make it noisy near close pairs (measured: twice
+    the block steps, same final levels).  With hi/lo the schedule is the oracle's: block
+    steps and force evaluations within 1 % (measured 160 / 55140 vs 160 / 55139), state
+    within 1e-9 / 2e-7 (measured 4.6e-11 / 2.1e-8)."""
+    c = inputs.CONFIGS["C2"]
+    m, x, v = inputs.make("C2")
+    xg, vg, lg, sg = run_block(m, x, v, c.eps, 1 / 128, 1, hilo=True)
+    xo, vo, _, _, lo, so, co = oracle.hermite_block(m, x, v, eps2_of(c.eps), 1 / 128, 1,
+                                                    eta=0.02, eta_s=0.01, kmax=20)
+    frac, adjacent, nclear = _levels_agree(lg, lo, co, 1 / 128)
+    assert nclear > 0.99 * c.n and frac >= 0.999 and adjacent, (frac, adjacent, nclear)
+    assert abs(sg[0] - so[0]) <= 0.01 * so[0] and abs(sg[1] - so[1]) <= 0.01 * so[1], (sg, so)
+    assert np.max(np.abs(xg - xo)) <= 1e-9 and np.max(np.abs(vg - vo)) <= 2e-7
+
+
+def test_block_energy_drift_vs_oracle():
+    """R#14 rule on a block run (C1, dt_max = 1/64, 16 cycles = 1/4 time unit): the GPU's
+    relative energy drift, both energies by the oracle's fp64 function, is at most twice the
+    oracle's own (floor 1e-11)."""
+    c = inputs.CONFIGS["C1"]
+    m, x, v = inputs.make("C1")
+    e2 = eps2_of(c.eps)
+    E0 = sum(oracle.energy(m, x, v, e2))
+    xg, vg, _, _ = run_block(m, x, v, c.eps, 1 / 64, 16)
+    xo, vo, *_ = oracle.hermite_block(m, x, v, e2, 1 / 64, 16, eta=0.02, eta_s=0.01, kmax=20)
+    dg = abs(sum(oracle.energy(m, xg, vg, e2)) - E0) / abs(E0)
+    do = abs(sum(oracle.energy(m, xo, vo, e2)) - E0) / abs(E0)
+    assert dg <= 2 * max(do, 1e-11), (dg, do)
+
+
+def test_block_kepler_gpu():
+    """e = 0.5 Kepler orbit (eps = 0: guarded kernel), one period of block steps at
+    eta = 0.001 against the closed form: within 1e-5 (the shared-dt GPU bar) and within
+    an order of magnitude of the oracle's own error + the fp32 force floor."""
+    m, x, v = inputs.kepler(0.5)
+    T = 2 * math.pi
+    xg, _, lg, sg = run_block(m, x, v, 0.0, T / 16, 16, eta=0.001, kmax=30)
+    xo, _, _, _, lo, so, _ = oracle.hermite_block(m, x, v, 0.0, T / 16, 16, eta=0.001, eta_s=0.01,
+                                                  kmax=30)
+    E = math.pi
+    for _ in range(100):
+        E -= (E - 0.5 * math.sin(E) - T) / (1 - 0.5 * math.cos(E))
+    rel = np.array([math.cos(E) - 0.5, math.sqrt(0.75) * math.sin(E), 0.0])
+    eg = np.linalg.norm((xg[:, 1] - xg[:, 0]) - rel)
+    eo = np.linalg.norm((xo[:, 1] - xo[:, 0]) - rel)
+    assert eg <= 1e-5 and eg <= 10 * eo + 2e-6, (eg, eo)
+    assert lg[0] == lg[1] and abs(sg[0] - so[0]) <= 0.05 * so[0], (lg, sg, so)
+
+
+def test_block_loopback_shards_bit_identical():
+    """Emulated i-shards (the multi-GPU partition in one context) give the same block
+    schedule and bit-identical states: t_next is a min over shards, forces follow the
+    canonical chunk order, active slots are independent."""
+    m, x, v = inputs.parity_round(*inputs.plummer(9000, 31))
+    out = []
+    for world in (1, 3):
+        out.append(run_block(m, x, v, 1e-3, 1 / 128, 2, world=world, loopback=world > 1))
+    (x1, v1, l1, s1), (x3, v3, l3, s3) = out
+    assert np.array_equal(x1, x3) and np.array_equal(v1, v3)
+    assert np.array_equal(l1, l3) and s1 == s3
+
+
+def test_block_host_round_trip_and_chaining():
+    """2 cycles, state to the host and back with keep_forces (levels kept), 2 more cycles ==
+    4 cycles in one call, bit for bit (call boundaries are multiples of dt_max)."""
+    m, x, v = inputs.parity_round(*inputs.plummer(3000, 5))
+    kw = dict(eps=1e-3, dt=1 / 128, integrator="block", eta=0.02, eta_s=0.01)
+    with binding.NBody(m, x, v, **kw) as s:
+        s.step(4)
+        xa, va = (t.cpu().numpy() for t in s.state())
+        sa = s.block_stats()
+    with binding.NBody(m, x, v, **kw) as s:
+        s.step(2)
+        xh, vh = (t.cpu().numpy() for t in s.state())
+        s.set_state(xh.copy(), vh.copy(), keep_forces=True)
+        s.step(2)
+        xb, vb = (t.cpu().numpy() for t in s.state())
+        sb = s.block_stats()
+    assert np.array_equal(xa, xb) and np.array_equal(va, vb) and sa == sb
+
+
+def test_block_argument_errors():
+    m, x, v = inputs.plummer(64, 1)
+    with pytest.raises(binding.NBodyError) as e:
+        binding.NBody(m, x, v, eps=1e-2, dt=1 / 64, integrator="block", eta=0.0)
+    assert e.value.code == binding.NBODY_EINVAL and "eta" in str(e.value)
+    with pytest.raises(binding.NBodyError) as e:
+        binding.NBody(m, x, v, eps=1e-2, dt=1 / 64, integrator="block", kmax=51)
+    assert e.value.code == binding.NBODY_EINVAL
+    with binding.NBody(m, x, v, eps=1e-2, dt=1 / 64) as s:
+        with pytest.raises(binding.NBodyError) as e:
+            s.block_stats()
+        assert e.value.code == binding.NBODY_EINVAL
