@@ -30,7 +30,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 # executed FP32 flops per interaction, FFMA = 2 (R#20; ncu-checked)
-FLOPS = {"hermite": 40, "leapfrog": 18}
+FLOPS = {"hermite": 40, "leapfrog": 18, "block": 40}
 FP32_LANES_PER_SM = 128      # FP32 FMA lanes per SM (4 SMSP x 32)
 
 
@@ -40,7 +40,12 @@ def parse():
     p.add_argument("--steps", type=int, default=10)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--config", default="C4")
-    p.add_argument("--integrator", default="hermite", choices=["hermite", "leapfrog"])
+    p.add_argument("--integrator", default="hermite", choices=["hermite", "leapfrog", "block"])
+    p.add_argument("--dt-max", type=float, default=1.0 / 128,
+                   help="block time steps: largest step dt_max (one bench step = dt_max of time)")
+    p.add_argument("--eta", type=float, default=0.02, help="block time steps: Aarseth eta")
+    p.add_argument("--hilo", default="auto", choices=["auto", "on", "off"],
+                   help="two-float positions (NEXT f2); auto = on for block time steps only")
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -263,9 +268,23 @@ def main():
         dist.broadcast_object_list(obj, src=0)
         nccl_id = obj[0]
 
-    sim = binding.NBody(mt, xt, vt, eps=c.eps, dt=c.dt, rank=rank, world=world,
-                        nccl_id=nccl_id, device=local, integrator=args.integrator)
-    FLOPS_PER_INTERACTION = FLOPS[args.integrator]
+    block = args.integrator == "block"
+    hilo = args.hilo == "on" or (args.hilo == "auto" and block)
+    sim = binding.NBody(mt, xt, vt, eps=c.eps, dt=args.dt_max if block else c.dt, rank=rank,
+                        world=world, nccl_id=nccl_id, device=local, integrator=args.integrator,
+                        eta=args.eta, hilo=hilo)
+
+    def active_sum():
+        """Block time steps: force evaluations so far, summed over ranks (each active
+        particle costs N interactions); None for the shared-dt integrators."""
+        if not block:
+            return None
+        a = torch.tensor([float(sim.block_stats()[1])], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(a, op=dist.ReduceOp.SUM)
+        return a.item()
+    # hi/lo positions add 6 FADD per interaction (d = (xj_hi - xi_hi) + (xj_lo - xi_lo))
+    FLOPS_PER_INTERACTION = FLOPS[args.integrator] + (6 if hilo else 0)
     stream = torch.cuda.current_stream(dev)
     flush = None if args.no_flush else torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
@@ -286,6 +305,8 @@ def main():
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
     barrier()
+    act0 = active_sum()
+    bs0 = sim.block_stats()[0] if block else None
     clocks.start()
     meter.start()
     for k in range(args.steps):
@@ -299,6 +320,8 @@ def main():
     clk = clocks.stop()
     sim.sync()
     ms_steps = sum(a.elapsed_time(b) for a, b in ev)
+    act_a = (active_sum() - act0) if block else None
+    block_steps_a = (sim.block_stats()[0] - bs0) if block else None
     if world > 1:   # whole-job GPU energy: sum over ranks (NaN marks a rank without a reading)
         ej = torch.tensor([energy["gpu_joules"] if energy["gpu_joules"] is not None else float("nan")],
                           dtype=torch.float64, device=dev)
@@ -310,6 +333,7 @@ def main():
     #      launch with CUDA events on the stream that launches it
     sim.prof_enable(True)
     barrier()
+    act1 = active_sum()
     for k in range(args.steps):
         if flush is not None:
             flush.zero_()
@@ -317,12 +341,14 @@ def main():
     barrier()
     force_ms, force_launches, _ = sim.prof_read(reset=True)
     sim.prof_enable(False)
+    act_b = (active_sum() - act1) if block else None
     t_local = torch.tensor([ms_steps, force_ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
     ms_total, force_ms_max = t_local.tolist()
     ms_per_step = ms_total / args.steps
-    interactions = float(n) * float(n) * args.steps
+    # interactions per pass: N^2 per shared step; block steps: N per active particle
+    interactions = float(n) * act_a if block else float(n) * float(n) * args.steps
     value = interactions / (ms_total * 1e-3)
 
     # ---- roofline of the dominant kernel (force pass): FP32 FMA pipe
@@ -332,7 +358,8 @@ def main():
     peak_tflops = sm_count * FP32_LANES_PER_SM * 2 * sm_max * 1e6 / 1e12
     n_loc = sim.n_loc
     force_launch_ms = force_ms / max(1, force_launches)
-    flops_per_launch = FLOPS_PER_INTERACTION * float(n_loc) * float(n) * args.steps / max(1, force_launches)
+    i_evals_b = (act_b / world) if block else float(n_loc) * args.steps   # this rank's i per pass
+    flops_per_launch = FLOPS_PER_INTERACTION * i_evals_b * float(n) / max(1, force_launches)
     achieved = flops_per_launch / (force_launch_ms * 1e-3) / 1e12 if force_launch_ms > 0 else None
     traffic = None
     try:
@@ -357,6 +384,7 @@ def main():
         barrier()
         t0 = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)
+        act2 = active_sum()
         t0.record(stream)
         for k in range(args.steps):
             binding._check(lib.nbody_set_state(sim_h._ctx, hx.data_ptr(), hv.data_ptr(), 1), sim_h._ctx)
@@ -367,7 +395,8 @@ def main():
         e_ms = torch.tensor([t0.elapsed_time(t1)], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
-        e2e = {"value": interactions / (e_ms.item() * 1e-3), "unit": "interactions/s",
+        inter_e = float(n) * (active_sum() - act2) if block else interactions
+        e2e = {"value": inter_e / (e_ms.item() * 1e-3), "unit": "interactions/s",
                "h2d_bytes_per_step": int(2 * 3 * 8 * (i1 - i0)) * world,
                "d2h_bytes_per_step": int(2 * 3 * 8 * (i1 - i0)) * world}
 
@@ -391,15 +420,23 @@ def main():
             "dtype": "f32",
             "data": "synthetic",
             "config": {
-                "workload": f"{args.config}: {c.kind} N={n} eps={c.eps} dt=1/1024, " + (
-                    "Hermite-4 P(EC)^1 step (predict, all-gather, acc+jerk force, correct)"
+                "workload": f"{args.config}: {c.kind} N={n} eps={c.eps} " + (
+                    "dt=1/1024, Hermite-4 P(EC)^1 step (predict, all-gather, acc+jerk force, correct)"
                     if args.integrator == "hermite" else
-                    "kick-drift-kick leapfrog step (kick+drift, all-gather, acc force, kick)"),
+                    "dt=1/1024, kick-drift-kick leapfrog step (kick+drift, all-gather, acc force, kick)"
+                    if args.integrator == "leapfrog" else
+                    f"block time steps, one step = dt_max = {args.dt_max:g} of individual Hermite-4 "
+                    f"steps (eta = {args.eta:g}, eta_s = 0.01): t_next, active set, predict all, "
+                    f"all-gather, force on the active set, correct + new levels")
+                + (", hi/lo positions" if hilo else ""),
                 "integrator": args.integrator,
                 "n": n, "flops_per_interaction": FLOPS_PER_INTERACTION,
                 "l2": "flushed between steps (256 MiB memset outside the per-step events)"
                       if flush is not None else "not flushed",
                 "parallelism": f"i-shard x{world}",
+                **({"block_steps_per_step": block_steps_a / args.steps,
+                    "mean_active": act_a / max(1, block_steps_a),
+                    "force_evaluations_per_step": act_a / args.steps} if block else {}),
             },
             "tflops": value * FLOPS_PER_INTERACTION / 1e12,
             "frac_fp32_peak": value * FLOPS_PER_INTERACTION / 1e12 / peak_tflops,
@@ -415,7 +452,7 @@ def main():
             "clocks": clk,
             "energy": dict(energy, joules_per_step=(energy["gpu_joules"] / args.steps
                                                     if energy["gpu_joules"] is not None else None),
-                           interactions_per_joule=(float(n) * n * args.steps / energy["gpu_joules"]
+                           interactions_per_joule=(interactions / energy["gpu_joules"]
                                                    if energy["gpu_joules"] else None),
                            scope=f"{world} GPU(s), NVML total-energy counter, summed over ranks, timed region"),
             "gpu_launches": launches,

@@ -152,7 +152,7 @@ class NBody:
     """
 
     def __init__(self, m, x, v, eps, dt, G=1.0, integrator="hermite", rank=0, world=1,
-                 loopback=False, nccl_id=None, device=None, stream=None, jchunks=0, hilo=False,
+                 loopback=False, nccl_id=None, device=None, stream=None, jchunks=0, hilo=None,
                  eta=0.02, eta_s=0.01, kmax=20):
         import torch
         if not torch.cuda.is_available():
@@ -168,6 +168,11 @@ class NBody:
         self._keep = []
         m, x, v = (self._prep(a) for a in (m, x, v))
         n = int(m.shape[0])
+        if hilo is None:
+            # block time steps difference forces over dt^2..dt^3 for the Aarseth
+            # criterion; fp32-rounded positions make it noisy (R#28), so
+            # two-float positions are the default there
+            hilo = integrator == "block"
         cfg = Config(n=n, G=float(G), eps=float(eps), dt=float(dt),
                      integrator=INTEGRATORS[integrator],
                      device=int(device), rank=int(rank), world=int(world),

@@ -26,6 +26,9 @@
 //            set, R#28); only the i prologue and the eps = 0 report see it
 #include "internal.h"
 
+#include <cstdlib>
+#include <cstring>
+
 namespace nb {
 
 namespace {
@@ -69,24 +72,35 @@ namespace {
 #define FK_EMPTYBAR 0    // 1: per-stage "empty" mbarriers (one arrive per warp) instead of a CTA barrier per tile
 #endif
 
-constexpr int kThreads = FK_THREADS;
-constexpr int kPairs = FK_PAIRS;          // i-pairs per thread (2 * kPairs i)
 constexpr int kStages = FK_STAGES;        // smem ring depth (tiles)
 constexpr int kUnroll = FK_UNROLL;
-constexpr int kHyb = FK_HYB;              // fp64 i per thread (FP64 pipe, runs beside FFMA2)
-constexpr int kIPerBlock = (2 * kPairs + kHyb) * kThreads;
 constexpr int kTileBytes = kTile * (int)sizeof(JPkt);
 constexpr int kLoTileBytes = kTile * (int)sizeof(float4);   // hi/lo position tails (NEXT f2)
-constexpr int kT64TileBytes = kHyb ? kTile * (int)sizeof(JPkt64) : 0;   // fp64 j tiles
-constexpr int kAccSmemBytes = FK_ACC_SMEM ? 6 * 2 * kPairs * kThreads * 8 : 0;
-// shared memory layout: [ring: kStages j-tiles][ring_lo: kStages lo-tiles][64 B mbarriers][fp64 acc]
-constexpr int kOffLo = kStages * kTileBytes;
-constexpr int kOff64 = kOffLo + kStages * kLoTileBytes;
-constexpr int kOffBar = kOff64 + kStages * kT64TileBytes;
-constexpr int kOffAcc = kOffBar + 64;
-constexpr int kSmemBytes = kOffAcc + kAccSmemBytes;
 static_assert(kStages * 8 * (FK_EMPTYBAR ? 2 : 1) <= 64, "mbarrier area");
-static_assert(!FK_EMPTYBAR || (kStages >= 3 && kHyb == 0), "empty-barrier ring: >= 3 stages, no fp64 share");
+
+// CTA shape: P packed i-pairs per thread, T threads, MINB resident CTAs per SM
+// (launch bounds), HYB fp64 i per thread.  Two shapes are instantiated: the
+// default (1024 i per CTA) and a small one (256 i per CTA) for launches with
+// few i -- block-step active sets and small N -- where 1024-i CTAs would leave
+// most SMs idle.  Every i's j loop is identical in both, so results are too.
+template <int P, int T, int MINB, int MINB_ACC, int HYB>
+struct FkCfg {
+    static constexpr int kPairs = P, kThreads = T, kMinB = MINB, kMinBAcc = MINB_ACC, kHyb = HYB;
+    static constexpr int kIPerBlock = (2 * P + HYB) * T;
+    static constexpr int kT64TileBytes = HYB ? kTile * (int)sizeof(JPkt64) : 0;   // fp64 j tiles
+    static constexpr int kAccSmemBytes = FK_ACC_SMEM ? 6 * 2 * P * T * 8 : 0;
+    // shared memory: [ring: kStages j-tiles][ring_lo: kStages lo-tiles][fp64 tiles][64 B mbarriers][fp64 acc]
+    static constexpr int kOffLo = kStages * kTileBytes;
+    static constexpr int kOff64 = kOffLo + kStages * kLoTileBytes;
+    static constexpr int kOffBar = kOff64 + kStages * kT64TileBytes;
+    static constexpr int kOffAcc = kOffBar + 64;
+    static constexpr int kSmemBytes = kOffAcc + kAccSmemBytes;
+    static_assert(!FK_EMPTYBAR || (kStages >= 3 && HYB == 0), "empty-barrier ring: >= 3 stages, no fp64 share");
+};
+using CfgBig = FkCfg<FK_PAIRS, FK_THREADS, FK_MINB, FK_MINB_ACC, FK_HYB>;
+using CfgSmall = FkCfg<1, 128, 6, 6, 0>;
+constexpr int kIPerBlock = CfgBig::kIPerBlock;
+constexpr int kHyb = CfgBig::kHyb;
 
 typedef unsigned long long f2;  // packed {lo, hi} fp32 pair in one 64-bit register
 
@@ -167,8 +181,11 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t
         : "memory");
 }
 
-template <bool kGuard, bool kJerk, bool kHiLo>
-__global__ void __launch_bounds__(kThreads, kJerk ? FK_MINB : FK_MINB_ACC) force_kernel(ForceArgs a) {
+template <bool kGuard, bool kJerk, bool kHiLo, class C, bool kList = false>
+__global__ void __launch_bounds__(C::kThreads, kJerk ? C::kMinB : C::kMinBAcc) force_kernel(ForceArgs a) {
+    constexpr int kPairs = C::kPairs, kThreads = C::kThreads, kHyb = C::kHyb;
+    constexpr int kIPerBlock = C::kIPerBlock, kT64TileBytes = C::kT64TileBytes;
+    constexpr int kOffLo = C::kOffLo, kOff64 = C::kOff64, kOffBar = C::kOffBar, kOffAcc = C::kOffAcc;
     constexpr int kNC = kJerk ? 6 : 3;   // accumulated components: a (+ jerk)
     constexpr uint32_t kStageTx = kTileBytes + (kHiLo ? kLoTileBytes : 0) + kT64TileBytes;
     extern __shared__ __align__(128) unsigned char smem[];
@@ -194,7 +211,8 @@ __global__ void __launch_bounds__(kThreads, kJerk ? FK_MINB : FK_MINB_ACC) force
         for (int h = 0; h < 2; ++h) {
             const int il = ib + (2 * p + h) * kThreads + tid;
             if (il < a.n_loc) {
-                const int64_t src = a.i_base + (a.ilist ? a.ilist[il] : il);   // block steps: active slot
+                int64_t src = a.i_base + il;
+                if constexpr (kList) src = a.i_base + a.ilist[il];   // block steps: active slot
                 const JPkt pk = a.pkt[src];
                 const float4 P = jpkt_pos(pk), V = jpkt_vel(pk);
                 q[h][0] = -P.x; q[h][1] = -P.y; q[h][2] = -P.z;
@@ -232,7 +250,7 @@ __global__ void __launch_bounds__(kThreads, kJerk ? FK_MINB : FK_MINB_ACC) force
     for (int h = 0; h < kHyb; ++h) {
         const int il = ib + (2 * kPairs + h) * kThreads + tid;
         if (il < a.n_loc) {
-            const JPkt64 pk = a.pk64[a.i_base + (a.ilist ? a.ilist[il] : il)];
+            const JPkt64 pk = a.pk64[a.i_base + (kList ? a.ilist[il] : il)];
             hx[h] = pk.p.x; hy[h] = pk.p.y; hz[h] = pk.p.z;
             hvx[h] = pk.v.x; hvy[h] = pk.v.y; hvz[h] = pk.v.z;
         } else {
@@ -373,14 +391,14 @@ __global__ void __launch_bounds__(kThreads, kJerk ? FK_MINB : FK_MINB_ACC) force
                     if (s_lo == 0.f) {
                         r_lo = 0.f;
                         const int sl = ib + (2 * p) * kThreads + tid;
-                        const int64_t ig = a.i_base + (a.ilist && sl < a.n_loc ? a.ilist[sl] : sl);
+                        const int64_t ig = a.i_base + (kList && sl < a.n_loc ? a.ilist[sl] : sl);
                         if (ig != jg && sl < a.n_loc && jmass != 0.f)
                             atomicMin(a.coincident, (unsigned long long)ig);
                     }
                     if (s_hi == 0.f) {
                         r_hi = 0.f;
                         const int sl = ib + (2 * p + 1) * kThreads + tid;
-                        const int64_t ig = a.i_base + (a.ilist && sl < a.n_loc ? a.ilist[sl] : sl);
+                        const int64_t ig = a.i_base + (kList && sl < a.n_loc ? a.ilist[sl] : sl);
                         if (ig != jg && sl < a.n_loc && jmass != 0.f)
                             atomicMin(a.coincident, (unsigned long long)ig);
                     }
@@ -427,7 +445,7 @@ __global__ void __launch_bounds__(kThreads, kJerk ? FK_MINB : FK_MINB_ACC) force
                         if (s == 0.0) {
                             ri = 0.0;
                             const int sl = ib + (2 * kPairs + h) * kThreads + tid;
-                            const int64_t ig = a.i_base + (a.ilist && sl < a.n_loc ? a.ilist[sl] : sl);
+                            const int64_t ig = a.i_base + (kList && sl < a.n_loc ? a.ilist[sl] : sl);
                             const int64_t jg = jc0 + (int64_t)t * kTile + jj;
                             if (ig != jg && sl < a.n_loc && Pd.w != 0.0)
                                 atomicMin(a.coincident, (unsigned long long)ig);
@@ -516,49 +534,98 @@ __global__ void __launch_bounds__(kThreads, kJerk ? FK_MINB : FK_MINB_ACC) force
 int force_i_per_block() { return kIPerBlock; }
 int force_hyb() { return kHyb; }
 
-
-template <bool G, bool J, bool H>
+template <bool G, bool J, bool H, class C>
 cudaError_t set_attr() {
-    return cudaFuncSetAttribute(force_kernel<G, J, H>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                kSmemBytes);
+    cudaError_t e = cudaFuncSetAttribute(force_kernel<G, J, H, C>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
+    if (e == cudaSuccess && J)   // active-list variant (block time steps use the jerk kernel)
+        e = cudaFuncSetAttribute(force_kernel<G, J, H, C, J>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
+    return e;
+}
+
+template <class C>
+cudaError_t set_attrs() {
+    cudaError_t e = cudaSuccess, r;
+    if ((r = set_attr<false, false, false, C>()) != cudaSuccess) e = r;
+    if ((r = set_attr<false, false, true, C>()) != cudaSuccess) e = r;
+    if ((r = set_attr<false, true, false, C>()) != cudaSuccess) e = r;
+    if ((r = set_attr<false, true, true, C>()) != cudaSuccess) e = r;
+    if ((r = set_attr<true, false, false, C>()) != cudaSuccess) e = r;
+    if ((r = set_attr<true, false, true, C>()) != cudaSuccess) e = r;
+    if ((r = set_attr<true, true, false, C>()) != cudaSuccess) e = r;
+    if ((r = set_attr<true, true, true, C>()) != cudaSuccess) e = r;
+    return e;
 }
 
 // dynamic shared memory above 48 KiB must be opted into once per instantiation
 cudaError_t ensure_attrs() {
     static cudaError_t done = [] {
-        cudaError_t e = cudaSuccess, r;
-        if ((r = set_attr<false, false, false>()) != cudaSuccess) e = r;
-        if ((r = set_attr<false, false, true>()) != cudaSuccess) e = r;
-        if ((r = set_attr<false, true, false>()) != cudaSuccess) e = r;
-        if ((r = set_attr<false, true, true>()) != cudaSuccess) e = r;
-        if ((r = set_attr<true, false, false>()) != cudaSuccess) e = r;
-        if ((r = set_attr<true, false, true>()) != cudaSuccess) e = r;
-        if ((r = set_attr<true, true, false>()) != cudaSuccess) e = r;
-        if ((r = set_attr<true, true, true>()) != cudaSuccess) e = r;
-        return e;
+        cudaError_t e = set_attrs<CfgBig>(), r = set_attrs<CfgSmall>();
+        return e != cudaSuccess ? e : r;
     }();
     return done;
 }
 
-template <bool G, bool J, bool H>
-cudaError_t launch_one(const ForceArgs& a, dim3 grid, cudaStream_t s) {
+template <bool G, bool J, bool H, class C>
+cudaError_t launch_one(const ForceArgs& a, unsigned c_count, cudaStream_t s) {
     cudaError_t e = ensure_attrs();
     if (e != cudaSuccess) return e;
-    force_kernel<G, J, H><<<grid, kThreads, kSmemBytes, s>>>(a);
+    const dim3 grid((unsigned)((a.n_loc + C::kIPerBlock - 1) / C::kIPerBlock), c_count);
+    // the active-list indirection is a separate instantiation so that the plain
+    // kernels' register allocation (and speed) is untouched by it
+    if (a.ilist) {
+        if constexpr (J) force_kernel<G, J, H, C, true><<<grid, C::kThreads, C::kSmemBytes, s>>>(a);
+        else return cudaErrorInvalidValue;   // block time steps always evaluate the jerk
+    } else {
+        force_kernel<G, J, H, C><<<grid, C::kThreads, C::kSmemBytes, s>>>(a);
+    }
     return cudaGetLastError();
 }
 
-template <bool G, bool J>
-cudaError_t launch_gj(const ForceArgs& a, dim3 grid, cudaStream_t s) {
-    return a.pklo ? launch_one<G, J, true>(a, grid, s) : launch_one<G, J, false>(a, grid, s);
+template <bool G, bool J, class C>
+cudaError_t launch_gj(const ForceArgs& a, cudaStream_t s) {
+    return a.pklo ? launch_one<G, J, true, C>(a, (unsigned)a.c_count, s)
+                  : launch_one<G, J, false, C>(a, (unsigned)a.c_count, s);
+}
+
+template <class C>
+cudaError_t launch_cfg(const ForceArgs& a, bool guard_self, bool jerk, cudaStream_t s) {
+    if (jerk) return guard_self ? launch_gj<true, true, C>(a, s) : launch_gj<false, true, C>(a, s);
+    return guard_self ? launch_gj<true, false, C>(a, s) : launch_gj<false, false, C>(a, s);
+}
+
+int sm_count() {
+    static int n = [] {
+        int dev = 0, v = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess ||
+            cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
+            cudaGetLastError();
+            return 148;
+        }
+        return v;
+    }();
+    return n;
+}
+
+// The small CTA shape when the default one would fill fewer than two waves of
+// the GPU (its per-CTA efficiency is within ~10 % of the default's,
+// profiles/r01_sweep_force.txt p1b6, and it quarters the idle i-slots).
+bool use_small_cta(const ForceArgs& a) {
+    if (kHyb != 0) return false;
+    const char* ov = getenv("NBODY_FORCE_CTA");   // tests: small | big (default: by size)
+    if (ov && !strcmp(ov, "small")) return true;
+    if (ov && !strcmp(ov, "big")) return false;
+    const int64_t ctas = (int64_t)((a.n_loc + kIPerBlock - 1) / kIPerBlock) * a.c_count;
+    return ctas < 2LL * FK_MINB * sm_count();
 }
 
 cudaError_t launch_force(const ForceArgs& a, bool guard_self, bool jerk, cudaStream_t s) {
     if (a.c_count <= 0 || a.n_loc <= 0) return cudaSuccess;
-    dim3 grid((unsigned)((a.n_loc + kIPerBlock - 1) / kIPerBlock), (unsigned)a.c_count);
-    if (jerk)
-        return guard_self ? launch_gj<true, true>(a, grid, s) : launch_gj<false, true>(a, grid, s);
-    return guard_self ? launch_gj<true, false>(a, grid, s) : launch_gj<false, false>(a, grid, s);
+#ifndef FK_NO_SMALL
+    if (use_small_cta(a)) return launch_cfg<CfgSmall>(a, guard_self, jerk, s);
+#endif
+    return launch_cfg<CfgBig>(a, guard_self, jerk, s);
 }
 
 int force_ctas_per_sm(bool jerk, bool hilo) {
@@ -568,12 +635,13 @@ int force_ctas_per_sm(bool jerk, bool hilo) {
         cudaGetLastError();
         return FK_MINB;
     }
+    constexpr int kT = CfgBig::kThreads, kS = CfgBig::kSmemBytes;
     if (jerk)
-        e = hilo ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, force_kernel<false, true, true>, kThreads, kSmemBytes)
-                 : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, force_kernel<false, true, false>, kThreads, kSmemBytes);
+        e = hilo ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, force_kernel<false, true, true, CfgBig>, kT, kS)
+                 : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, force_kernel<false, true, false, CfgBig>, kT, kS);
     else
-        e = hilo ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, force_kernel<false, false, true>, kThreads, kSmemBytes)
-                 : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, force_kernel<false, false, false>, kThreads, kSmemBytes);
+        e = hilo ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, force_kernel<false, false, true, CfgBig>, kT, kS)
+                 : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, force_kernel<false, false, false, CfgBig>, kT, kS);
     if (e != cudaSuccess) {
         cudaGetLastError();
         return FK_MINB;

@@ -39,7 +39,7 @@ def test_block_reduces_to_shared_step_bitwise():
     corrector), so the states are bit-identical."""
     c = inputs.CONFIGS["C1"]
     m, x, v = inputs.make("C1")
-    xb, vb, lev, st = run_block(m, x, v, c.eps, c.dt, 4, eta=1e30, eta_s=1e30)
+    xb, vb, lev, st = run_block(m, x, v, c.eps, c.dt, 4, eta=1e30, eta_s=1e30, hilo=False)
     with binding.NBody(m, x, v, eps=c.eps, dt=c.dt) as s:
         s.step(4)
         xs, vs = (t.cpu().numpy() for t in s.state())
@@ -64,7 +64,7 @@ def test_block_trajectory_levels_and_steps_vs_oracle():
     c = inputs.CONFIGS["C1"]
     m, x, v = inputs.make("C1")
     dt_max, ncyc = 1 / 64, 4
-    xg, vg, lg, sg = run_block(m, x, v, c.eps, dt_max, ncyc)
+    xg, vg, lg, sg = run_block(m, x, v, c.eps, dt_max, ncyc, hilo=False)
     xo, vo, _, _, lo, so, co = oracle.hermite_block(m, x, v, eps2_of(c.eps), dt_max, ncyc,
                                                     eta=0.02, eta_s=0.01, kmax=20)
     assert lo.max() - lo.min() >= 3                       # genuinely individual steps
@@ -171,3 +171,22 @@ def test_block_argument_errors():
         with pytest.raises(binding.NBodyError) as e:
             s.block_stats()
         assert e.value.code == binding.NBODY_EINVAL
+
+
+@pytest.mark.parametrize("n", [1000, 5000])
+def test_force_cta_shapes_bit_identical(n, monkeypatch):
+    """Force launches over few i (block-step active sets, small N) run the 256-i CTA
+    shape, large ones the 1024-i shape (NBODY_FORCE_CTA=small|big overrides the choice).
+    Each i's j loop is the same in both, so forces are bit-identical, and the small shape
+    meets the parity bar against the oracle."""
+    m, x, v = inputs.parity_round(*inputs.plummer(n, 77))
+    out = {}
+    for shape in ("small", "big"):
+        monkeypatch.setenv("NBODY_FORCE_CTA", shape)
+        with binding.NBody(m, x, v, eps=1e-3, dt=1 / 64, hilo=False) as s:
+            out[shape] = [t.cpu().numpy() for t in s.forces()]
+    assert np.array_equal(out["small"][0], out["big"][0])
+    assert np.array_equal(out["small"][1], out["big"][1])
+    ao, jo = oracle.forces(m, x, v, eps2_of(1e-3))
+    from metrics import max_rel
+    assert max_rel(out["small"][0], ao) <= 1e-5 and max_rel(out["small"][1], jo) <= 1e-4
