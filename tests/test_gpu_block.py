@@ -190,3 +190,14 @@ def test_force_cta_shapes_bit_identical(n, monkeypatch):
     ao, jo = oracle.forces(m, x, v, eps2_of(1e-3))
     from metrics import max_rel
     assert max_rel(out["small"][0], ao) <= 1e-5 and max_rel(out["small"][1], jo) <= 1e-4
+
+
+def test_block_nccl_single_rank_communicator():
+    """world = 1 with an NCCL id runs the multi-rank block path for real: t_next through
+    ncclAllReduce(min), packets through ncclAllGather (in place).  Same schedule and
+    bit-identical states as the communicator-free path."""
+    m, x, v = inputs.parity_round(*inputs.plummer(5000, 9))
+    plain = run_block(m, x, v, 1e-3, 1 / 128, 2)
+    nccl = run_block(m, x, v, 1e-3, 1 / 128, 2, nccl_id=binding.nccl_unique_id())
+    assert np.array_equal(plain[0], nccl[0]) and np.array_equal(plain[1], nccl[1])
+    assert np.array_equal(plain[2], nccl[2]) and plain[3] == nccl[3]
