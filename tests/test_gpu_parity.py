@@ -88,6 +88,19 @@ def test_config_forces_sampled(cfg):
     check_forces(m, x, v, c.eps, idx=idx)
 
 
+def test_large_ragged_n_sampled_and_sharded():
+    """N = 300 001 (odd; chunk = 2560 j, the last chunk ragged; padding packets in the last
+    tile): R#11 sample against the oracle, and loopback world = 3 (ragged shards) equal to
+    world = 1 bit for bit."""
+    n = 300001
+    m, x, v = inputs.parity_round(*inputs.plummer(n, 41))
+    idx = sample_indices(x, n_stride=2048, n_special=128)
+    check_forces(m, x, v, 1e-3, idx=idx)
+    a1, j1 = gpu_forces(m, x, v, 1e-3)
+    a3, j3 = gpu_forces(m, x, v, 1e-3, world=3, loopback=True)
+    assert np.array_equal(a1, a3) and np.array_equal(j1, j3)
+
+
 def test_two_cluster_small_all_particles():
     m, x, v = inputs.parity_round(*inputs.two_cluster(8192, 4))
     check_forces(m, x, v, 1e-3)
