@@ -26,8 +26,11 @@
 //            set, R#28); only the i prologue and the eps = 0 report see it
 #include "internal.h"
 
+#include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <cstdio>
+#include <type_traits>
 
 namespace nb {
 
@@ -196,6 +199,26 @@ __global__ void __launch_bounds__(C::kThreads, kJerk ? C::kMinB : C::kMinBAcc) f
     [[maybe_unused]] uint64_t* empty = full + kStages;   // FK_EMPTYBAR: all warps done with a stage
 
     const int tid = threadIdx.x;
+    int n_loc = a.n_loc;
+    if constexpr (kList) n_loc = *a.n_dev;   // block steps: active count read on the device
+    // Active-list launches (block time steps) read the active count on the device; their
+    // grid (ceil(count / kIPerBlock), chunks) is set by the host or, inside the block-step
+    // CUDA graph, by the decide kernel (device-updatable node).  One CTA = one work item.
+    if constexpr (kList)
+        if ((int)blockIdx.x * kIPerBlock >= n_loc) return;
+
+    if (tid == 0) {
+#pragma unroll
+        for (int s = 0; s < kStages; ++s) mbar_init(&full[s], 1);
+#if FK_EMPTYBAR
+        for (int s = 0; s < kStages; ++s) mbar_init(&empty[s], kThreads / 32);
+#endif
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    const uint32_t tbase = 0;   // tiles consumed before this work item (ring stage and phase)
+    {
     const int c = (a.c_first + (int)blockIdx.y) % a.n_chunks;
     const int64_t jc0 = (int64_t)c * a.chunk;
     const int ntile = a.chunk / kTile;
@@ -210,7 +233,7 @@ __global__ void __launch_bounds__(C::kThreads, kJerk ? C::kMinB : C::kMinBAcc) f
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
             const int il = ib + (2 * p + h) * kThreads + tid;
-            if (il < a.n_loc) {
+            if (il < n_loc) {
                 int64_t src = a.i_base + il;
                 if constexpr (kList) src = a.i_base + a.ilist[il];   // block steps: active slot
                 const JPkt pk = a.pkt[src];
@@ -249,7 +272,7 @@ __global__ void __launch_bounds__(C::kThreads, kJerk ? C::kMinB : C::kMinBAcc) f
 #pragma unroll
     for (int h = 0; h < kHyb; ++h) {
         const int il = ib + (2 * kPairs + h) * kThreads + tid;
-        if (il < a.n_loc) {
+        if (il < n_loc) {
             const JPkt64 pk = a.pk64[a.i_base + (kList ? a.ilist[il] : il)];
             hx[h] = pk.p.x; hy[h] = pk.p.y; hz[h] = pk.p.z;
             hvx[h] = pk.v.x; hvy[h] = pk.v.y; hvz[h] = pk.v.z;
@@ -273,33 +296,26 @@ __global__ void __launch_bounds__(C::kThreads, kJerk ? C::kMinB : C::kMinBAcc) f
 #pragma unroll
         for (int l = 0; l < 2 * kPairs; ++l) ACC64(k, l) = 0.0;
 
-    if (tid == 0) {
-#pragma unroll
-        for (int s = 0; s < kStages; ++s) mbar_init(&full[s], 1);
-#if FK_EMPTYBAR
-        for (int s = 0; s < kStages; ++s) mbar_init(&empty[s], kThreads / 32);
-#endif
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    if (tid == 0) {
+    if (tid == 0) {   // the ring is free: every thread passed the previous item's last barrier
         for (int s = 0; s < kStages && s < ntile; ++s) {
-            mbar_expect_tx(&full[s], kStageTx);
-            tma_load_1d(ring + s * kTile, a.pkt + jc0 + (int64_t)s * kTile, kTileBytes, &full[s]);
+            const int st = (int)((tbase + s) % kStages);
+            mbar_expect_tx(&full[st], kStageTx);
+            tma_load_1d(ring + st * kTile, a.pkt + jc0 + (int64_t)s * kTile, kTileBytes, &full[st]);
             if (kHiLo)
-                tma_load_1d(ring_lo + s * kTile, a.pklo + jc0 + (int64_t)s * kTile, kLoTileBytes,
-                            &full[s]);
+                tma_load_1d(ring_lo + st * kTile, a.pklo + jc0 + (int64_t)s * kTile, kLoTileBytes,
+                            &full[st]);
             if (kHyb)
-                tma_load_1d(ring64 + s * kTile, a.pk64 + jc0 + (int64_t)s * kTile, kT64TileBytes,
-                            &full[s]);
+                tma_load_1d(ring64 + st * kTile, a.pk64 + jc0 + (int64_t)s * kTile, kT64TileBytes,
+                            &full[st]);
         }
     }
 
     const f2 m3 = f2bc(-3.0f);
 
     for (int t = 0; t < ntile; ++t) {
-        const int s = t % kStages;
-        mbar_wait(&full[s], (uint32_t)((t / kStages) & 1));
+        const uint32_t tg = tbase + t;
+        const int s = (int)(tg % kStages);
+        mbar_wait(&full[s], (tg / kStages) & 1);
         const JPkt* tile = ring + s * kTile;
         const float4* tile_lo = ring_lo + s * kTile;
         const JPkt64* tile64 = ring64 + s * kTile;
@@ -391,15 +407,15 @@ __global__ void __launch_bounds__(C::kThreads, kJerk ? C::kMinB : C::kMinBAcc) f
                     if (s_lo == 0.f) {
                         r_lo = 0.f;
                         const int sl = ib + (2 * p) * kThreads + tid;
-                        const int64_t ig = a.i_base + (kList && sl < a.n_loc ? a.ilist[sl] : sl);
-                        if (ig != jg && sl < a.n_loc && jmass != 0.f)
+                        const int64_t ig = a.i_base + (kList && sl < n_loc ? a.ilist[sl] : sl);
+                        if (ig != jg && sl < n_loc && jmass != 0.f)
                             atomicMin(a.coincident, (unsigned long long)ig);
                     }
                     if (s_hi == 0.f) {
                         r_hi = 0.f;
                         const int sl = ib + (2 * p + 1) * kThreads + tid;
-                        const int64_t ig = a.i_base + (kList && sl < a.n_loc ? a.ilist[sl] : sl);
-                        if (ig != jg && sl < a.n_loc && jmass != 0.f)
+                        const int64_t ig = a.i_base + (kList && sl < n_loc ? a.ilist[sl] : sl);
+                        if (ig != jg && sl < n_loc && jmass != 0.f)
                             atomicMin(a.coincident, (unsigned long long)ig);
                     }
                 }
@@ -445,9 +461,9 @@ __global__ void __launch_bounds__(C::kThreads, kJerk ? C::kMinB : C::kMinBAcc) f
                         if (s == 0.0) {
                             ri = 0.0;
                             const int sl = ib + (2 * kPairs + h) * kThreads + tid;
-                            const int64_t ig = a.i_base + (kList && sl < a.n_loc ? a.ilist[sl] : sl);
+                            const int64_t ig = a.i_base + (kList && sl < n_loc ? a.ilist[sl] : sl);
                             const int64_t jg = jc0 + (int64_t)t * kTile + jj;
-                            if (ig != jg && sl < a.n_loc && Pd.w != 0.0)
+                            if (ig != jg && sl < n_loc && Pd.w != 0.0)
                                 atomicMin(a.coincident, (unsigned long long)ig);
                         }
                     }
@@ -513,7 +529,7 @@ __global__ void __launch_bounds__(C::kThreads, kJerk ? C::kMinB : C::kMinBAcc) f
 #pragma unroll
     for (int l = 0; l < 2 * kPairs; ++l) {
         const int il = ib + l * kThreads + tid;
-        if (il < a.n_loc) {
+        if (il < n_loc) {
 #pragma unroll
             for (int k = 0; k < kNC; ++k) out[(int64_t)k * a.n_loc_pad + il] = ACC64(k, l);
         }
@@ -521,26 +537,31 @@ __global__ void __launch_bounds__(C::kThreads, kJerk ? C::kMinB : C::kMinBAcc) f
 #pragma unroll
     for (int h = 0; h < kHyb; ++h) {
         const int il = ib + (2 * kPairs + h) * kThreads + tid;
-        if (il < a.n_loc) {
+        if (il < n_loc) {
 #pragma unroll
             for (int k = 0; k < kNC; ++k) out[(int64_t)k * a.n_loc_pad + il] = hacc[k][h];
         }
     }
+    }   // work item
 #undef ACC64
 }
 
 }  // namespace
 
 int force_i_per_block() { return kIPerBlock; }
+int force_list_i_per_block() { return CfgSmall::kIPerBlock; }
 int force_hyb() { return kHyb; }
+
+int sm_count();
 
 template <bool G, bool J, bool H, class C>
 cudaError_t set_attr() {
     cudaError_t e = cudaFuncSetAttribute(force_kernel<G, J, H, C>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
-    if (e == cudaSuccess && J)   // active-list variant (block time steps use the jerk kernel)
-        e = cudaFuncSetAttribute(force_kernel<G, J, H, C, J>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
+    if constexpr (J && std::is_same<C, CfgSmall>::value)   // persistent active-list variant
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(force_kernel<G, J, H, C, true>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
     return e;
 }
 
@@ -571,12 +592,16 @@ template <bool G, bool J, bool H, class C>
 cudaError_t launch_one(const ForceArgs& a, unsigned c_count, cudaStream_t s) {
     cudaError_t e = ensure_attrs();
     if (e != cudaSuccess) return e;
-    const dim3 grid((unsigned)((a.n_loc + C::kIPerBlock - 1) / C::kIPerBlock), c_count);
     // the active-list indirection is a separate instantiation so that the plain
     // kernels' register allocation (and speed) is untouched by it
+    const dim3 grid((unsigned)std::max<int64_t>(1, (a.n_loc + C::kIPerBlock - 1) / C::kIPerBlock), c_count);
     if (a.ilist) {
-        if constexpr (J) force_kernel<G, J, H, C, true><<<grid, C::kThreads, C::kSmemBytes, s>>>(a);
-        else return cudaErrorInvalidValue;   // block time steps always evaluate the jerk
+        if constexpr (J && std::is_same<C, CfgSmall>::value) {
+            if (!a.n_dev) return cudaErrorInvalidValue;
+            force_kernel<G, J, H, C, true><<<grid, C::kThreads, C::kSmemBytes, s>>>(a);
+        } else {
+            return cudaErrorInvalidValue;   // block time steps: jerk kernel, small CTA shape
+        }
     } else {
         force_kernel<G, J, H, C><<<grid, C::kThreads, C::kSmemBytes, s>>>(a);
     }
@@ -622,6 +647,7 @@ bool use_small_cta(const ForceArgs& a) {
 
 cudaError_t launch_force(const ForceArgs& a, bool guard_self, bool jerk, cudaStream_t s) {
     if (a.c_count <= 0 || a.n_loc <= 0) return cudaSuccess;
+    if (a.ilist) return launch_cfg<CfgSmall>(a, guard_self, jerk, s);   // persistent list kernel
 #ifndef FK_NO_SMALL
     if (use_small_cta(a)) return launch_cfg<CfgSmall>(a, guard_self, jerk, s);
 #endif

@@ -247,9 +247,44 @@ __global__ void block_select_kernel(StateArgs a) {
     }
 }
 
+__global__ void block_begin_kernel(unsigned long long* tnext, int32_t* nact, int nshards) {
+    if (threadIdx.x == 0) *tnext = ~0ull;
+    for (int q = threadIdx.x; q < nshards; q += blockDim.x) nact[q] = 0;
+}
+
+__global__ void block_set_tend_kernel(long long* ctl, unsigned long long t_end) {
+    ctl[0] = (long long)t_end;
+    ctl[3] = 0;
+}
+
+__global__ void block_decide_kernel(long long* ctl, const unsigned long long* tnext, int32_t* nact,
+                                    int nshards, cudaGraphConditionalHandle cond,
+                                    const BlockGraphNodes* nodes) {
+    const bool done = *tnext > (unsigned long long)ctl[0];
+    if (done) {
+        for (int q = 0; q < nshards; ++q) nact[q] = 0;
+    } else {
+        long long na = 0;
+        for (int q = 0; q < nshards; ++q) na += nact[q];
+        ctl[1] += 1;
+        ctl[2] += na;
+    }
+    ctl[3] = done ? 1 : 0;
+    if (nodes) {   // inside the block-step graph
+        for (int q = 0; q < nshards; ++q) {
+            if (!nodes->force[q]) continue;   // shard without particles: no force node
+            const int nb = (nact[q] + nodes->i_per_block - 1) / nodes->i_per_block;
+            cudaGraphKernelNodeSetEnabled(nodes->force[q], nb > 0);
+            if (nb > 0) cudaGraphKernelNodeSetGridDim(nodes->force[q], dim3((unsigned)nb, (unsigned)nodes->chunks[q], 1));
+        }
+        cudaGraphSetConditional(cond, done ? 0u : 1u);
+    }
+}
+
 // every local particle predicted to t_next with its own polynomial (the
 // predictor of predict() with dt -> D = t_next - t_i), packed for the exchange
 __global__ void block_predict_pack_kernel(StateArgs a) {
+    if (a.ctl[3]) return;   // past t_end: this block step is a no-op
     const unsigned long long tn = *a.tnext;
     const double tick = ldexp(a.dt, -a.kmax);
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < a.n_loc; i += gridDim.x * blockDim.x) {
@@ -274,7 +309,8 @@ __global__ void block_predict_pack_kernel(StateArgs a) {
 // fold the active slots' chunk partials, Hermite corrector with the particle's
 // own dt_i (R#3 form), Aarseth criterion from a1, j1 and the interpolated
 // a^(2)(t_next) = a2 + dt a3, a^(3) = a3, block rules for the next level
-__global__ void block_correct_kernel(StateArgs a, int32_t n_act) {
+__global__ void block_correct_kernel(StateArgs a) {
+    const int32_t n_act = *a.nact;
     const unsigned long long tn = *a.tnext;
     for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n_act; q += gridDim.x * blockDim.x) {
         const int i = a.ilist[q];
@@ -372,9 +408,23 @@ cudaError_t launch_block_predict_pack(const StateArgs& a, cudaStream_t s) {
     block_predict_pack_kernel<<<grid_for(a.n_loc), kBlock, 0, s>>>(a);
     return cudaGetLastError();
 }
-cudaError_t launch_block_correct(const StateArgs& a, int32_t n_act, cudaStream_t s) {
-    if (n_act <= 0) return cudaSuccess;
-    block_correct_kernel<<<grid_for(n_act), kBlock, 0, s>>>(a, n_act);
+cudaError_t launch_block_correct(const StateArgs& a, cudaStream_t s) {
+    if (a.n_loc <= 0) return cudaSuccess;
+    block_correct_kernel<<<grid_for(a.n_loc), kBlock, 0, s>>>(a);
+    return cudaGetLastError();
+}
+cudaError_t launch_block_begin(unsigned long long* tnext, int32_t* nact, int nshards, cudaStream_t s) {
+    block_begin_kernel<<<1, 32, 0, s>>>(tnext, nact, nshards);
+    return cudaGetLastError();
+}
+cudaError_t launch_block_set_tend(long long* ctl, unsigned long long t_end, cudaStream_t s) {
+    block_set_tend_kernel<<<1, 1, 0, s>>>(ctl, t_end);
+    return cudaGetLastError();
+}
+cudaError_t launch_block_decide(long long* ctl, const unsigned long long* tnext, int32_t* nact,
+                                int nshards, cudaGraphConditionalHandle cond,
+                                const BlockGraphNodes* nodes, cudaStream_t s) {
+    block_decide_kernel<<<1, 1, 0, s>>>(ctl, tnext, nact, nshards, cond, nodes);
     return cudaGetLastError();
 }
 cudaError_t launch_fill_padding(JPkt* pkt, float4* pklo, JPkt64* pk64, int64_t from, int64_t to,

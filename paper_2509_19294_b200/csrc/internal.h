@@ -76,6 +76,8 @@ struct ForceArgs {
     unsigned long long* coincident;  // eps == 0 only: min global i of a coincident pair
     const int32_t* ilist;  // block steps: local index of the particle in i-slot il, or nullptr
                            // (slot il is particle il); partial rows are indexed by slot
+    const int32_t* n_dev;  // with ilist: the active count on the device (n_loc is then only an
+                           // upper bound sizing the persistent grid)
 };
 
 // Launches the force pass for chunks c_first .. c_first + c_count - 1 (mod
@@ -83,6 +85,7 @@ struct ForceArgs {
 // (leapfrog, NEXT f1; partial has 3 components).  Returns the launch error.
 cudaError_t launch_force(const ForceArgs& a, bool guard_self, bool jerk, cudaStream_t s);
 int force_i_per_block();
+int force_list_i_per_block();   // i per CTA of the active-list (block-step) force launches
 int force_hyb();   // fp64 i-particles per thread in the force kernel (0: pure FP32)
 // resident force CTAs per SM for the kernel variant (occupancy calculator)
 int force_ctas_per_sm(bool jerk, bool hilo);
@@ -110,6 +113,7 @@ struct StateArgs {
     int32_t* ilist;      // [n_loc] active particles (local indices), slot order
     int32_t* nact;       // active count (device counter)
     unsigned long long* tnext;  // next block time in ticks (device, shared by shards)
+    long long* ctl;      // block-run control [t_end ticks, block steps, sum of active, done]
     int32_t kmax;
     double eta, eta_s;
 };
@@ -135,8 +139,24 @@ cudaError_t launch_block_init_levels(const StateArgs& a, cudaStream_t s);  // le
 cudaError_t launch_block_reset_time(const StateArgs& a, cudaStream_t s);   // T = 0 (call start)
 cudaError_t launch_block_tnext(const StateArgs& a, cudaStream_t s);        // atomicMin(tnext, T + dt)
 cudaError_t launch_block_select(const StateArgs& a, cudaStream_t s);       // ilist, nact
+// reset t_next and the active counts of all nshards shards (start of a block step)
+cudaError_t launch_block_begin(unsigned long long* tnext, int32_t* nact, int nshards, cudaStream_t s);
+// ctl[0] = t_end (start of a call)
+cudaError_t launch_block_set_tend(long long* ctl, unsigned long long t_end, cudaStream_t s);
+// after t_next and the active sets: done = t_next > t_end (then the active counts are zeroed so
+// the rest of the block step is a no-op), statistics, and -- inside the block-step CUDA graph
+// -- the WHILE-loop condition and the grid (ceil(nact / i_per_block), chunks[q]) of every
+// shard's device-updatable force node (disabled when its active set is empty)
+struct BlockGraphNodes {
+    cudaGraphDeviceNode_t force[8];   // per shard (loopback shards <= 8 use the graph)
+    int32_t chunks[8];
+    int32_t i_per_block;
+};
+cudaError_t launch_block_decide(long long* ctl, const unsigned long long* tnext, int32_t* nact,
+                                int nshards, cudaGraphConditionalHandle cond,
+                                const BlockGraphNodes* nodes, cudaStream_t s);
 cudaError_t launch_block_predict_pack(const StateArgs& a, cudaStream_t s); // all -> t_next
-// correct the n_act active particles (n_act read on the host), new levels, T = t_next
-cudaError_t launch_block_correct(const StateArgs& a, int32_t n_act, cudaStream_t s);
+// correct the active particles (count read on the device), new levels, T = t_next
+cudaError_t launch_block_correct(const StateArgs& a, cudaStream_t s);
 
 }  // namespace nb

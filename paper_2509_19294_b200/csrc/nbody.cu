@@ -148,9 +148,11 @@ struct nbody_ctx {
     // active counts, pinned read-back of both, run statistics
     unsigned long long* tnext = nullptr;
     int32_t* nact = nullptr;
+    nb::BlockGraphNodes* gnodes = nullptr;   // device copy of the graph's force-node handles
+    long long* ctl = nullptr;            // [t_end, block steps, active sum, done] (device)
     void* hbuf = nullptr;
     bool levels_ok = false;
-    int64_t block_steps = 0, active_sum = 0;
+    cudaGraphExec_t block_graph = nullptr;   // WHILE-loop graph of block steps (R#28)
     cudaStream_t stream = nullptr, comm_stream = nullptr;
     bool own_stream = false;
     cudaEvent_t ev_packed = nullptr, ev_gathered = nullptr;
@@ -232,6 +234,7 @@ nb::StateArgs state_args(nbody_ctx* c, Shard& s) {
     a.ilist = s.ilist;
     a.nact = c->nact ? c->nact + (&s - c->sh.data()) : nullptr;
     a.tnext = c->tnext;
+    a.ctl = c->ctl;
     a.kmax = c->cfg.kmax;
     a.eta = c->cfg.eta;
     a.eta_s = c->cfg.eta_s;
@@ -243,7 +246,7 @@ bool use_nccl(const nbody_ctx* c) { return c->comm != nullptr; }
 // force pass over chunks [c_first, c_first + c_count) for the shard's local
 // particles, or (block steps) for the n_i active particles listed in ilist
 int launch_force_range(nbody_ctx* c, Shard& s, int32_t c_first, int32_t c_count, int32_t n_i = -1,
-                       const int32_t* ilist = nullptr) {
+                       const int32_t* ilist = nullptr, const int32_t* n_dev = nullptr) {
     if (n_i < 0) n_i = s.n_loc;
     if (c_count <= 0 || n_i <= 0) return NBODY_OK;
     nb::ForceArgs f;
@@ -253,6 +256,7 @@ int launch_force_range(nbody_ctx* c, Shard& s, int32_t c_first, int32_t c_count,
     f.i_base = s.plan.i0;
     f.n_loc = n_i;
     f.ilist = ilist;
+    f.n_dev = n_dev;
     f.n_loc_pad = s.n_loc_pad;
     f.chunk = (int32_t)s.plan.chunk;
     f.n_chunks = (int32_t)s.plan.n_chunks;
@@ -405,6 +409,9 @@ void free_ctx(nbody_ctx* c) {
     }
     cudaFree(c->tnext);
     cudaFree(c->nact);
+    cudaFree(c->ctl);
+    cudaFree(c->gnodes);
+    if (c->block_graph) cudaGraphExecDestroy(c->block_graph);
     if (c->hbuf) cudaFreeHost(c->hbuf);
     cudaFree(c->pkt);
     cudaFree(c->pklo);
@@ -487,7 +494,10 @@ int init_impl(const nbody_config* cfg, const double* m, const double* x, const d
     if (nb::force_hyb() > 0 && (rc = dalloc(c, &c->pk64, (size_t)c->L))) return rc;
     if ((rc = dalloc(c, &c->flags, 4))) return rc;
     if (is_block(c)) {
-        if ((rc = dalloc(c, &c->tnext, 1)) || (rc = dalloc(c, &c->nact, (size_t)c->nshards))) return rc;
+        if ((rc = dalloc(c, &c->tnext, 1)) || (rc = dalloc(c, &c->nact, (size_t)c->nshards)) ||
+            (rc = dalloc(c, &c->ctl, 4)) || (rc = dalloc(c, &c->gnodes, 1)))
+            return rc;
+        CK(c, cudaMemsetAsync(c->ctl, 0, 4 * sizeof(long long), c->stream));
         CK(c, cudaMallocHost(&c->hbuf, 8 + 4 * (size_t)c->nshards));
     }
     CK(c, cudaMemsetAsync(c->flags, 0xff, 4 * sizeof(unsigned long long), c->stream));
@@ -634,11 +644,58 @@ int one_step(nbody_ctx* c) {
 }  // namespace
 
 namespace {
-// Block time steps (R#28): nsteps * dt_max of individual Hermite steps.  Per
-// block step: t_next = min(t_i + dt_i) (device reduction, NCCL min over ranks),
-// active list, predict + pack everything, exchange, force pass on the active
-// slots only, correct + new level.  t_next and the active counts come back to
-// the host each block step: they end the loop and size the force grid.
+// Block time steps (R#28): nsteps * dt_max of individual Hermite steps.  One block
+// step: reset counters, t_next = min(t_i + dt_i) (device reduction, NCCL min over
+// ranks), active lists, decide (done = t_next > t_end; statistics), predict + pack
+// everything, exchange, persistent force pass over the active slots (device count),
+// correct + new levels.  No launch needs a host-side count, so without NCCL the whole
+// loop is one CUDA graph with a WHILE node whose condition the decide kernel sets;
+// with NCCL (or kernel timing on) the host drives the loop and reads `done`.
+int block_step_body(nbody_ctx* c, cudaGraphConditionalHandle cond, const nb::BlockGraphNodes* nodes) {
+    int rc;
+    CK(c, nb::launch_block_begin(c->tnext, c->nact, c->nshards, c->stream));
+    for (auto& s : c->sh) CK(c, nb::launch_block_tnext(state_args(c, s), c->stream));
+    if (use_nccl(c))
+        CKNCCL(c, nccl().AllReduce(c->tnext, c->tnext, 1, ncclUint64, ncclMin, c->comm, c->stream));
+    for (auto& s : c->sh) CK(c, nb::launch_block_select(state_args(c, s), c->stream));
+    CK(c, nb::launch_block_decide(c->ctl, c->tnext, c->nact, c->nshards, cond, nodes, c->stream));
+    return NBODY_OK;
+}
+
+// predict, exchange, force on the active sets, correct.  Host loop: n_act[q] are the
+// active counts read back.  Graph capture (n_act == nullptr): every force launch is made
+// device-updatable and its handle recorded in *nodes for the decide kernel.
+int block_step_rest(nbody_ctx* c, const int32_t* n_act, nb::BlockGraphNodes* nodes) {
+    int rc;
+    for (auto& s : c->sh) CK(c, nb::launch_block_predict_pack(state_args(c, s), c->stream));
+    if (use_nccl(c) && (rc = gather_packets(c, c->stream))) return rc;
+    for (int q = 0; q < c->nshards; ++q) {
+        Shard& s = c->sh[q];
+        const int32_t n_i = n_act ? n_act[q] : std::max<int32_t>(1, s.n_loc);
+        if (n_i <= 0 || s.n_loc <= 0) continue;
+        if ((rc = launch_force_range(c, s, 0, (int32_t)s.plan.n_chunks, n_i, s.ilist, c->nact + q)))
+            return rc;
+        if (nodes) {
+            cudaStreamCaptureStatus st;
+            const cudaGraphNode_t* deps = nullptr;
+            size_t nd = 0;
+            CK(c, cudaStreamGetCaptureInfo(c->stream, &st, nullptr, nullptr, &deps, &nd));
+            if (st != cudaStreamCaptureStatusActive || nd != 1)
+                return fail(c, NBODY_ECUDA, "block graph: force node not found in the capture");
+            cudaLaunchAttributeValue av = {};
+            av.deviceUpdatableKernelNode.deviceUpdatable = 1;
+            CK(c, cudaGraphKernelNodeSetAttribute(deps[0], cudaLaunchAttributeDeviceUpdatableKernelNode, &av));
+            cudaLaunchAttributeValue got = {};
+            CK(c, cudaGraphKernelNodeGetAttribute(deps[0], cudaLaunchAttributeDeviceUpdatableKernelNode, &got));
+            nodes->force[q] = got.deviceUpdatableKernelNode.devNode;
+            nodes->chunks[q] = (int32_t)s.plan.n_chunks;
+        }
+    }
+    for (auto& s : c->sh) CK(c, nb::launch_block_correct(state_args(c, s), c->stream));
+    c->n_kernels += 4 + 4 * (int64_t)c->nshards;
+    return NBODY_OK;
+}
+
 int block_run(nbody_ctx* c, int32_t nsteps) {
     int rc;
     const int kmax = c->cfg.kmax;
@@ -653,43 +710,65 @@ int block_run(nbody_ctx* c, int32_t nsteps) {
         c->n_kernels++;
     }
     c->levels_ok = true;
-    const unsigned long long T_end = (unsigned long long)nsteps << kmax;
-    unsigned long long* h_tnext = reinterpret_cast<unsigned long long*>(c->hbuf);
+    CK(c, nb::launch_block_set_tend(c->ctl, (unsigned long long)nsteps << kmax, c->stream));
+    const bool graph_ok = !use_nccl(c) && !c->prof && c->use_graph && c->nshards <= 8 &&
+                          c->stream != cudaStreamLegacy && c->stream != cudaStreamPerThread &&
+                          c->stream != nullptr;
+    if (graph_ok) {
+        if (!c->block_graph) {
+            cudaGraph_t g = nullptr;
+            CK(c, cudaGraphCreate(&g, 0));
+            cudaGraphConditionalHandle cond;
+            cudaGraphNodeParams cp = {};
+            cudaGraphNode_t node;
+            cudaError_t e = cudaGraphConditionalHandleCreate(&cond, g, 1, cudaGraphCondAssignDefault);
+            if (e == cudaSuccess) {
+                cp.type = cudaGraphNodeTypeConditional;
+                cp.conditional.handle = cond;
+                cp.conditional.type = cudaGraphCondTypeWhile;
+                cp.conditional.size = 1;
+                e = cudaGraphAddNode(&node, g, nullptr, 0, &cp);
+            }
+            if (e == cudaSuccess)
+                e = cudaStreamBeginCaptureToGraph(c->stream, cp.conditional.phGraph_out[0], nullptr, nullptr,
+                                                  0, cudaStreamCaptureModeThreadLocal);
+            if (e != cudaSuccess) {
+                cudaGraphDestroy(g);
+                CK(c, e);
+            }
+            const int64_t nk0 = c->n_kernels, nf0 = c->n_force;
+            nb::BlockGraphNodes hn = {};
+            hn.i_per_block = nb::force_list_i_per_block();
+            rc = block_step_body(c, cond, c->gnodes);
+            if (!rc) rc = block_step_rest(c, nullptr, &hn);
+            cudaGraph_t body = nullptr;
+            e = cudaStreamEndCapture(c->stream, &body);
+            c->n_kernels = nk0;
+            c->n_force = nf0;
+            if (rc || e != cudaSuccess) {
+                cudaGraphDestroy(g);
+                if (rc) return rc;
+                CK(c, e);
+            }
+            e = cudaGraphInstantiate(&c->block_graph, g, 0);
+            cudaGraphDestroy(g);
+            CK(c, e);
+            CK(c, cudaMemcpyAsync(c->gnodes, &hn, sizeof hn, cudaMemcpyHostToDevice, c->stream));
+            CK(c, cudaStreamSynchronize(c->stream));   // hn is a stack object
+        }
+        CK(c, cudaGraphLaunch(c->block_graph, c->stream));
+        return NBODY_OK;
+    }
+    // host-driven loop (NCCL ranks, kernel timing, no capturable stream)
+    long long* h_done = reinterpret_cast<long long*>(c->hbuf);
     int32_t* h_nact = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(c->hbuf) + 8);
     for (;;) {
-        CK(c, cudaMemsetAsync(c->tnext, 0xff, sizeof(unsigned long long), c->stream));
-        CK(c, cudaMemsetAsync(c->nact, 0, sizeof(int32_t) * c->nshards, c->stream));
-        for (auto& s : c->sh) {
-            CK(c, nb::launch_block_tnext(state_args(c, s), c->stream));
-            c->n_kernels++;
-        }
-        if (use_nccl(c))
-            CKNCCL(c, nccl().AllReduce(c->tnext, c->tnext, 1, ncclUint64, ncclMin, c->comm, c->stream));
-        for (auto& s : c->sh) {
-            CK(c, nb::launch_block_select(state_args(c, s), c->stream));
-            c->n_kernels++;
-        }
-        CK(c, cudaMemcpyAsync(c->hbuf, c->tnext, 8, cudaMemcpyDeviceToHost, c->stream));
+        if ((rc = block_step_body(c, cudaGraphConditionalHandle{}, nullptr))) return rc;
+        CK(c, cudaMemcpyAsync(h_done, c->ctl + 3, sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
         CK(c, cudaMemcpyAsync(h_nact, c->nact, 4 * (size_t)c->nshards, cudaMemcpyDeviceToHost, c->stream));
         CK(c, cudaStreamSynchronize(c->stream));
-        if (*h_tnext > T_end) break;
-        for (auto& s : c->sh) {
-            CK(c, nb::launch_block_predict_pack(state_args(c, s), c->stream));
-            c->n_kernels++;
-        }
-        if (use_nccl(c) && (rc = gather_packets(c, c->stream))) return rc;
-        int64_t na = 0;
-        for (int q = 0; q < c->nshards; ++q) {
-            Shard& s = c->sh[q];
-            if ((rc = launch_force_range(c, s, 0, (int32_t)s.plan.n_chunks, h_nact[q], s.ilist))) return rc;
-            na += h_nact[q];
-        }
-        for (int q = 0; q < c->nshards; ++q) {
-            CK(c, nb::launch_block_correct(state_args(c, c->sh[q]), h_nact[q], c->stream));
-            c->n_kernels++;
-        }
-        c->block_steps++;
-        c->active_sum += na;
+        if (*h_done) break;
+        if ((rc = block_step_rest(c, h_nact, nullptr))) return rc;
     }
     return NBODY_OK;
 }
@@ -836,9 +915,11 @@ int nbody_block_stats(nbody_ctx* c, int64_t* block_steps, int64_t* active_sum, i
                 CK(c, cudaMemcpyAsync(level + (s.plan.i0 - k0), s.lev, 4 * (size_t)s.n_loc, cudaMemcpyDefault,
                                       c->stream));
     }
+    long long h[4];
+    CK(c, cudaMemcpyAsync(h, c->ctl, sizeof h, cudaMemcpyDeviceToHost, c->stream));
     CK(c, cudaStreamSynchronize(c->stream));
-    if (block_steps) *block_steps = c->block_steps;
-    if (active_sum) *active_sum = c->active_sum;
+    if (block_steps) *block_steps = h[1];
+    if (active_sum) *active_sum = h[2];
     return NBODY_OK;
 }
 
