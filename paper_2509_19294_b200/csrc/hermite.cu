@@ -235,18 +235,6 @@ __global__ void block_tnext_kernel(StateArgs a) {
     if ((threadIdx.x & 31) == 0 && best != ~0ull) atomicMin(a.tnext, best);
 }
 
-// active set {i : t_i + dt_i == t_next}; slot order is irrelevant to the
-// results (every slot's force is the same j-loop), so an atomic append suffices
-__global__ void block_select_kernel(StateArgs a) {
-    const unsigned long long tn = *a.tnext;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < a.n_loc; i += gridDim.x * blockDim.x) {
-        if ((unsigned long long)(a.T[i] + ticks_of(a, a.lev[i])) == tn) {
-            const int slot = atomicAdd(a.nact, 1);
-            a.ilist[slot] = i;
-        }
-    }
-}
-
 __global__ void block_begin_kernel(unsigned long long* tnext, int32_t* nact, int nshards) {
     if (threadIdx.x == 0) *tnext = ~0ull;
     for (int q = threadIdx.x; q < nshards; q += blockDim.x) nact[q] = 0;
@@ -281,13 +269,18 @@ __global__ void block_decide_kernel(long long* ctl, const unsigned long long* tn
     }
 }
 
-// every local particle predicted to t_next with its own polynomial (the
-// predictor of predict() with dt -> D = t_next - t_i), packed for the exchange
-__global__ void block_predict_pack_kernel(StateArgs a) {
-    if (a.ctl[3]) return;   // past t_end: this block step is a no-op
+// active set {i : t_i + dt_i == t_next} (atomic append: slot order is irrelevant to the
+// results, every slot's force is the same j loop) and every local particle predicted to t_next with
+// its own polynomial (the predictor of predict() with dt -> D = t_next - t_i), packed for
+// the exchange.  In the block step past t_end the prediction is scratch nobody reads.
+__global__ void block_select_predict_kernel(StateArgs a) {
     const unsigned long long tn = *a.tnext;
     const double tick = ldexp(a.dt, -a.kmax);
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < a.n_loc; i += gridDim.x * blockDim.x) {
+        if ((unsigned long long)(a.T[i] + ticks_of(a, a.lev[i])) == tn) {
+            const int slot = atomicAdd(a.nact, 1);
+            a.ilist[slot] = i;
+        }
         const double D = (double)(int64_t)(tn - (unsigned long long)a.T[i]) * tick;
         const double D2 = D * D, D3 = D2 * D;
         double xp[3], vp[3];
@@ -309,7 +302,7 @@ __global__ void block_predict_pack_kernel(StateArgs a) {
 // fold the active slots' chunk partials, Hermite corrector with the particle's
 // own dt_i (R#3 form), Aarseth criterion from a1, j1 and the interpolated
 // a^(2)(t_next) = a2 + dt a3, a^(3) = a3, block rules for the next level
-__global__ void block_correct_kernel(StateArgs a) {
+__global__ void block_correct_kernel(StateArgs a, int32_t* reset_nact, int reset_n, int32_t* done_ctas) {
     const int32_t n_act = *a.nact;
     const unsigned long long tn = *a.tnext;
     for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n_act; q += gridDim.x * blockDim.x) {
@@ -347,6 +340,20 @@ __global__ void block_correct_kernel(StateArgs a) {
         }
         a.lev[i] = kn;
         a.T[i] = (int64_t)tn;
+    }
+    // the last CTA of the last shard's launch resets t_next and the active counts for the
+    // next block step (every CTA has read them by the time it counts itself done)
+    if (reset_nact) {
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            if (atomicAdd(done_ctas, 1) == (int)gridDim.x - 1) {
+                *a.tnext = ~0ull;
+                for (int q = 0; q < reset_n; ++q) reset_nact[q] = 0;
+                *done_ctas = 0;
+                __threadfence();
+            }
+        }
     }
 }
 
@@ -398,19 +405,15 @@ cudaError_t launch_block_tnext(const StateArgs& a, cudaStream_t s) {
     block_tnext_kernel<<<grid_for(a.n_loc), kBlock, 0, s>>>(a);
     return cudaGetLastError();
 }
-cudaError_t launch_block_select(const StateArgs& a, cudaStream_t s) {
+cudaError_t launch_block_select_predict(const StateArgs& a, cudaStream_t s) {
     if (a.n_loc <= 0) return cudaSuccess;
-    block_select_kernel<<<grid_for(a.n_loc), kBlock, 0, s>>>(a);
+    block_select_predict_kernel<<<grid_for(a.n_loc), kBlock, 0, s>>>(a);
     return cudaGetLastError();
 }
-cudaError_t launch_block_predict_pack(const StateArgs& a, cudaStream_t s) {
-    if (a.n_loc <= 0) return cudaSuccess;
-    block_predict_pack_kernel<<<grid_for(a.n_loc), kBlock, 0, s>>>(a);
-    return cudaGetLastError();
-}
-cudaError_t launch_block_correct(const StateArgs& a, cudaStream_t s) {
-    if (a.n_loc <= 0) return cudaSuccess;
-    block_correct_kernel<<<grid_for(a.n_loc), kBlock, 0, s>>>(a);
+cudaError_t launch_block_correct(const StateArgs& a, int32_t* reset_nact, int reset_n, int32_t* done_ctas,
+                                 cudaStream_t s) {
+    block_correct_kernel<<<grid_for(a.n_loc > 0 ? a.n_loc : 1), kBlock, 0, s>>>(a, reset_nact, reset_n,
+                                                                                   done_ctas);
     return cudaGetLastError();
 }
 cudaError_t launch_block_begin(unsigned long long* tnext, int32_t* nact, int nshards, cudaStream_t s) {

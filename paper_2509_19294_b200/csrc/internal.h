@@ -138,8 +138,7 @@ int energy_blocks(int32_t n_loc);
 cudaError_t launch_block_init_levels(const StateArgs& a, cudaStream_t s);  // lev from eta_s, T = 0
 cudaError_t launch_block_reset_time(const StateArgs& a, cudaStream_t s);   // T = 0 (call start)
 cudaError_t launch_block_tnext(const StateArgs& a, cudaStream_t s);        // atomicMin(tnext, T + dt)
-cudaError_t launch_block_select(const StateArgs& a, cudaStream_t s);       // ilist, nact
-// reset t_next and the active counts of all nshards shards (start of a block step)
+// reset t_next and the active counts of all nshards shards
 cudaError_t launch_block_begin(unsigned long long* tnext, int32_t* nact, int nshards, cudaStream_t s);
 // ctl[0] = t_end (start of a call)
 cudaError_t launch_block_set_tend(long long* ctl, unsigned long long t_end, cudaStream_t s);
@@ -155,8 +154,12 @@ struct BlockGraphNodes {
 cudaError_t launch_block_decide(long long* ctl, const unsigned long long* tnext, int32_t* nact,
                                 int nshards, cudaGraphConditionalHandle cond,
                                 const BlockGraphNodes* nodes, cudaStream_t s);
-cudaError_t launch_block_predict_pack(const StateArgs& a, cudaStream_t s); // all -> t_next
-// correct the active particles (count read on the device), new levels, T = t_next
-cudaError_t launch_block_correct(const StateArgs& a, cudaStream_t s);
+// active set + every particle predicted to t_next and packed (one pass)
+cudaError_t launch_block_select_predict(const StateArgs& a, cudaStream_t s);
+// correct the active particles (count read on the device), new levels, T = t_next; with
+// reset_nact != nullptr its last CTA resets t_next and reset_nact[0 .. reset_n) for the next
+// block step (done_ctas: zero-initialised CTA counter)
+cudaError_t launch_block_correct(const StateArgs& a, int32_t* reset_nact, int reset_n, int32_t* done_ctas,
+                                 cudaStream_t s);
 
 }  // namespace nb

@@ -149,6 +149,7 @@ struct nbody_ctx {
     unsigned long long* tnext = nullptr;
     int32_t* nact = nullptr;
     nb::BlockGraphNodes* gnodes = nullptr;   // device copy of the graph's force-node handles
+    int32_t* done_ctas = nullptr;            // last-CTA counter of the correct kernel
     long long* ctl = nullptr;            // [t_end, block steps, active sum, done] (device)
     void* hbuf = nullptr;
     bool levels_ok = false;
@@ -411,6 +412,7 @@ void free_ctx(nbody_ctx* c) {
     cudaFree(c->nact);
     cudaFree(c->ctl);
     cudaFree(c->gnodes);
+    cudaFree(c->done_ctas);
     if (c->block_graph) cudaGraphExecDestroy(c->block_graph);
     if (c->hbuf) cudaFreeHost(c->hbuf);
     cudaFree(c->pkt);
@@ -495,9 +497,11 @@ int init_impl(const nbody_config* cfg, const double* m, const double* x, const d
     if ((rc = dalloc(c, &c->flags, 4))) return rc;
     if (is_block(c)) {
         if ((rc = dalloc(c, &c->tnext, 1)) || (rc = dalloc(c, &c->nact, (size_t)c->nshards)) ||
-            (rc = dalloc(c, &c->ctl, 4)) || (rc = dalloc(c, &c->gnodes, 1)))
+            (rc = dalloc(c, &c->ctl, 4)) || (rc = dalloc(c, &c->gnodes, 1)) ||
+            (rc = dalloc(c, &c->done_ctas, 1)))
             return rc;
         CK(c, cudaMemsetAsync(c->ctl, 0, 4 * sizeof(long long), c->stream));
+        CK(c, cudaMemsetAsync(c->done_ctas, 0, sizeof(int32_t), c->stream));
         CK(c, cudaMallocHost(&c->hbuf, 8 + 4 * (size_t)c->nshards));
     }
     CK(c, cudaMemsetAsync(c->flags, 0xff, 4 * sizeof(unsigned long long), c->stream));
@@ -651,13 +655,14 @@ namespace {
 // correct + new levels.  No launch needs a host-side count, so without NCCL the whole
 // loop is one CUDA graph with a WHILE node whose condition the decide kernel sets;
 // with NCCL (or kernel timing on) the host drives the loop and reads `done`.
+// t_next and the active counts start reset (block_begin before the first block step, then
+// the last CTA of each block step's corrector)
 int block_step_body(nbody_ctx* c, cudaGraphConditionalHandle cond, const nb::BlockGraphNodes* nodes) {
     int rc;
-    CK(c, nb::launch_block_begin(c->tnext, c->nact, c->nshards, c->stream));
     for (auto& s : c->sh) CK(c, nb::launch_block_tnext(state_args(c, s), c->stream));
     if (use_nccl(c))
         CKNCCL(c, nccl().AllReduce(c->tnext, c->tnext, 1, ncclUint64, ncclMin, c->comm, c->stream));
-    for (auto& s : c->sh) CK(c, nb::launch_block_select(state_args(c, s), c->stream));
+    for (auto& s : c->sh) CK(c, nb::launch_block_select_predict(state_args(c, s), c->stream));
     CK(c, nb::launch_block_decide(c->ctl, c->tnext, c->nact, c->nshards, cond, nodes, c->stream));
     return NBODY_OK;
 }
@@ -667,7 +672,6 @@ int block_step_body(nbody_ctx* c, cudaGraphConditionalHandle cond, const nb::Blo
 // device-updatable and its handle recorded in *nodes for the decide kernel.
 int block_step_rest(nbody_ctx* c, const int32_t* n_act, nb::BlockGraphNodes* nodes) {
     int rc;
-    for (auto& s : c->sh) CK(c, nb::launch_block_predict_pack(state_args(c, s), c->stream));
     if (use_nccl(c) && (rc = gather_packets(c, c->stream))) return rc;
     for (int q = 0; q < c->nshards; ++q) {
         Shard& s = c->sh[q];
@@ -691,8 +695,12 @@ int block_step_rest(nbody_ctx* c, const int32_t* n_act, nb::BlockGraphNodes* nod
             nodes->chunks[q] = (int32_t)s.plan.n_chunks;
         }
     }
-    for (auto& s : c->sh) CK(c, nb::launch_block_correct(state_args(c, s), c->stream));
-    c->n_kernels += 4 + 4 * (int64_t)c->nshards;
+    for (int q = 0; q < c->nshards; ++q) {
+        const bool last = q == c->nshards - 1;
+        CK(c, nb::launch_block_correct(state_args(c, c->sh[q]), last ? c->nact : nullptr, c->nshards,
+                                       c->done_ctas, c->stream));
+    }
+    c->n_kernels += 1 + 4 * (int64_t)c->nshards;
     return NBODY_OK;
 }
 
@@ -711,6 +719,7 @@ int block_run(nbody_ctx* c, int32_t nsteps) {
     }
     c->levels_ok = true;
     CK(c, nb::launch_block_set_tend(c->ctl, (unsigned long long)nsteps << kmax, c->stream));
+    CK(c, nb::launch_block_begin(c->tnext, c->nact, c->nshards, c->stream));
     const bool graph_ok = !use_nccl(c) && !c->prof && c->use_graph && c->nshards <= 8 &&
                           c->stream != cudaStreamLegacy && c->stream != cudaStreamPerThread &&
                           c->stream != nullptr;
