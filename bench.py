@@ -178,10 +178,23 @@ def cpu_baseline(m, x, v, eps2, budget_s):
     t0 = time.perf_counter()
     oracle.forces(m, x, v, eps2, idx=idx)
     el = time.perf_counter() - t0
-    return {"value": ns * n / el, "unit": "interactions/s", "cores": oracle.threads(),
+    cores = oracle.threads()
+    # the same oracle on one core, on an eighth of the time budget
+    n1 = max(16, int(ns * (budget_s / 8) / max(el * cores, 1e-4)))
+    idx1 = np.linspace(0, n - 1, min(n, n1)).astype(np.int64)
+    oracle.set_threads(1)
+    try:
+        t0 = time.perf_counter()
+        oracle.forces(m, x, v, eps2, idx=idx1)
+        el1 = time.perf_counter() - t0
+    finally:
+        oracle.set_threads(cores)
+    return {"value": ns * n / el, "unit": "interactions/s", "cores": cores,
             "kind": "oracle",
             "sample": f"acc+jerk of {ns} evenly strided i against all {n} j (fp64, OpenMP over i); "
-                      f"{el:.1f} s"}
+                      f"{el:.1f} s",
+            "value_1core": len(idx1) * n / el1,
+            "sample_1core": f"{len(idx1)} strided i against all {n} j on 1 thread; {el1:.1f} s"}
 
 
 def run_reference(args):
