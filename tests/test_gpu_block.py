@@ -201,3 +201,39 @@ def test_block_nccl_single_rank_communicator():
     nccl = run_block(m, x, v, 1e-3, 1 / 128, 2, nccl_id=binding.nccl_unique_id())
     assert np.array_equal(plain[0], nccl[0]) and np.array_equal(plain[1], nccl[1])
     assert np.array_equal(plain[2], nccl[2]) and plain[3] == nccl[3]
+
+
+def test_block_kmax_cap_and_compute_forces_mid_run():
+    """kmax = 2 caps the levels (the criterion would go deeper) and the run still ends
+    synchronised with every level <= 2; nbody_compute_forces between calls returns the
+    forces at the synchronised state (oracle parity) and keeps the levels."""
+    m, x, v = inputs.parity_round(*inputs.plummer(2000, 13))
+    with binding.NBody(m, x, v, eps=1e-3, dt=1 / 16, integrator="block", kmax=2) as s:
+        s.step(2)
+        steps, active, lev = s.block_stats(levels=True)
+        assert lev.max() <= 2 and steps <= 2 * 4 and active >= 2 * 2000
+        xs, vs = (t.cpu().numpy() for t in s.state())
+        a, j = (t.cpu().numpy() for t in s.forces())
+        _, _, lev2 = s.block_stats(levels=True)
+        assert np.array_equal(lev, lev2)
+        s.step(1)
+        s.sync()
+    ao, jo = oracle.forces(m, xs, vs, eps2_of(1e-3))
+    from metrics import max_rel
+    # states are off the fp32 grid here; hi/lo positions keep the force error ~1e-6
+    assert max_rel(a, ao) <= 1e-5 and max_rel(j, jo) <= 1e-4
+
+
+def test_block_coincident_pair_eps0_is_reported():
+    """eps = 0 with two particles on the same spot: the guarded list kernel reports the
+    coincident pair as NBODY_ENONFINITE at the next blocking call (sticky afterwards)."""
+    m, x, v = inputs.parity_round(*inputs.uniform_cube(300, 5))
+    x[:, 17] = x[:, 200]
+    with binding.NBody(m, x, v, eps=0.0, dt=1 / 64, integrator="block") as s:
+        with pytest.raises(binding.NBodyError) as e:
+            s.step(1)
+            s.sync()
+        assert e.value.code == binding.NBODY_ENONFINITE
+        with pytest.raises(binding.NBodyError) as e2:
+            s.step(1)
+        assert e2.value.code == binding.NBODY_ESTATE
