@@ -68,18 +68,12 @@ namespace {
 #ifndef FK_ACC_SMEM
 #define FK_ACC_SMEM 1
 #endif
-#ifndef FK_PREFETCH
-#define FK_PREFETCH 0    // 1: j packet of the next j loaded into registers one iteration ahead
-#endif
-#ifndef FK_EMPTYBAR
-#define FK_EMPTYBAR 0    // 1: per-stage "empty" mbarriers (one arrive per warp) instead of a CTA barrier per tile
-#endif
 
 constexpr int kStages = FK_STAGES;        // smem ring depth (tiles)
 constexpr int kUnroll = FK_UNROLL;
 constexpr int kTileBytes = kTile * (int)sizeof(JPkt);
 constexpr int kLoTileBytes = kTile * (int)sizeof(float4);   // hi/lo position tails (NEXT f2)
-static_assert(kStages * 8 * (FK_EMPTYBAR ? 2 : 1) <= 64, "mbarrier area");
+static_assert(kStages * 8 <= 64, "mbarrier area");
 
 // CTA shape: P packed i-pairs per thread, T threads, MINB resident CTAs per SM
 // (launch bounds), HYB fp64 i per thread.  Two shapes are instantiated: the
@@ -98,7 +92,6 @@ struct FkCfg {
     static constexpr int kOffBar = kOff64 + kStages * kT64TileBytes;
     static constexpr int kOffAcc = kOffBar + 64;
     static constexpr int kSmemBytes = kOffAcc + kAccSmemBytes;
-    static_assert(!FK_EMPTYBAR || (kStages >= 3 && HYB == 0), "empty-barrier ring: >= 3 stages, no fp64 share");
 };
 using CfgBig = FkCfg<FK_PAIRS, FK_THREADS, FK_MINB, FK_MINB_ACC, FK_HYB>;
 using CfgSmall = FkCfg<1, 128, 6, 6, 0>;
@@ -171,9 +164,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
             : "memory");
     }
 }
-[[maybe_unused]] __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
-}
 // 1-D bulk TMA global -> shared, completion counted on `bar` (UBLKCP in SASS)
 __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes,
                                             uint64_t* bar) {
@@ -196,7 +186,6 @@ __global__ void __launch_bounds__(C::kThreads, kJerk ? C::kMinB : C::kMinBAcc) f
     float4* ring_lo = reinterpret_cast<float4*>(smem + kOffLo);
     JPkt64* ring64 = reinterpret_cast<JPkt64*>(smem + kOff64);
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + kOffBar);
-    [[maybe_unused]] uint64_t* empty = full + kStages;   // FK_EMPTYBAR: all warps done with a stage
 
     const int tid = threadIdx.x;
     int n_loc = a.n_loc;
@@ -210,15 +199,10 @@ __global__ void __launch_bounds__(C::kThreads, kJerk ? C::kMinB : C::kMinBAcc) f
     if (tid == 0) {
 #pragma unroll
         for (int s = 0; s < kStages; ++s) mbar_init(&full[s], 1);
-#if FK_EMPTYBAR
-        for (int s = 0; s < kStages; ++s) mbar_init(&empty[s], kThreads / 32);
-#endif
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
 
-    const uint32_t tbase = 0;   // tiles consumed before this work item (ring stage and phase)
-    {
     const int c = (a.c_first + (int)blockIdx.y) % a.n_chunks;
     const int64_t jc0 = (int64_t)c * a.chunk;
     const int ntile = a.chunk / kTile;
@@ -296,34 +280,29 @@ __global__ void __launch_bounds__(C::kThreads, kJerk ? C::kMinB : C::kMinBAcc) f
 #pragma unroll
         for (int l = 0; l < 2 * kPairs; ++l) ACC64(k, l) = 0.0;
 
-    if (tid == 0) {   // the ring is free: every thread passed the previous item's last barrier
+    if (tid == 0) {
         for (int s = 0; s < kStages && s < ntile; ++s) {
-            const int st = (int)((tbase + s) % kStages);
-            mbar_expect_tx(&full[st], kStageTx);
-            tma_load_1d(ring + st * kTile, a.pkt + jc0 + (int64_t)s * kTile, kTileBytes, &full[st]);
+            mbar_expect_tx(&full[s], kStageTx);
+            tma_load_1d(ring + s * kTile, a.pkt + jc0 + (int64_t)s * kTile, kTileBytes, &full[s]);
             if (kHiLo)
-                tma_load_1d(ring_lo + st * kTile, a.pklo + jc0 + (int64_t)s * kTile, kLoTileBytes,
-                            &full[st]);
+                tma_load_1d(ring_lo + s * kTile, a.pklo + jc0 + (int64_t)s * kTile, kLoTileBytes,
+                            &full[s]);
             if (kHyb)
-                tma_load_1d(ring64 + st * kTile, a.pk64 + jc0 + (int64_t)s * kTile, kT64TileBytes,
-                            &full[st]);
+                tma_load_1d(ring64 + s * kTile, a.pk64 + jc0 + (int64_t)s * kTile, kT64TileBytes,
+                            &full[s]);
         }
     }
 
     const f2 m3 = f2bc(-3.0f);
 
     for (int t = 0; t < ntile; ++t) {
-        const uint32_t tg = tbase + t;
-        const int s = (int)(tg % kStages);
-        mbar_wait(&full[s], (tg / kStages) & 1);
+        const int s = t % kStages;
+        mbar_wait(&full[s], (uint32_t)((t / kStages) & 1));
         const JPkt* tile = ring + s * kTile;
         const float4* tile_lo = ring_lo + s * kTile;
         const JPkt64* tile64 = ring64 + s * kTile;
 #if defined(FK_EXP_NOLDS) && !NB_PKT_DUP
         float4 Pr = tile[0].p, Vr = tile[0].v;
-#endif
-#if FK_PREFETCH && !NB_PKT_DUP && !defined(FK_EXP_NOLDS)
-        float4 Pn = tile[0].p, Vn = tile[0].v;
 #endif
 
         f2 acc[kNC][kPairs];
@@ -359,17 +338,8 @@ __global__ void __launch_bounds__(C::kThreads, kJerk ? C::kMinB : C::kMinBAcc) f
             const float4 P = Pr;
             const float4 V = Vr;
 #else
-#if FK_PREFETCH
-            const float4 P = Pn, V = Vn;
-            {
-                const int jn = jj + 1 < kTile ? jj + 1 : jj;   // stays inside the stage
-                Pn = tile[jn].p;
-                Vn = tile[jn].v;
-            }
-#else
             const float4 P = tile[jj].p;
             const float4 V = tile[jj].v;
-#endif
 #endif
             const f2 xj = f2bc(P.x), yj = f2bc(P.y), zj = f2bc(P.z), mj = f2bc(P.w);
             const f2 eps2 = f2bc(V.w);
@@ -493,22 +463,6 @@ __global__ void __launch_bounds__(C::kThreads, kJerk ? C::kMinB : C::kMinBAcc) f
                 ACC64(k, 2 * p) += (double)lo;
                 ACC64(k, 2 * p + 1) += (double)hi;
             }
-#if FK_EMPTYBAR
-        // each warp releases stage s; thread 0 refills the stage released one tile
-        // earlier (t - 1), so only warp 0 waits, and only for the slowest warp's tile t - 1
-        __syncwarp();
-        if ((tid & 31) == 0) mbar_arrive(&empty[s]);
-        if (tid == 0 && t >= 1 && t - 1 + kStages < ntile) {
-            const int sp = (t - 1) % kStages;
-            mbar_wait(&empty[sp], (uint32_t)(((t - 1) / kStages) & 1));
-            mbar_expect_tx(&full[sp], kStageTx);
-            tma_load_1d(ring + sp * kTile, a.pkt + jc0 + (int64_t)(t - 1 + kStages) * kTile,
-                        kTileBytes, &full[sp]);
-            if (kHiLo)
-                tma_load_1d(ring_lo + sp * kTile, a.pklo + jc0 + (int64_t)(t - 1 + kStages) * kTile,
-                            kLoTileBytes, &full[sp]);
-        }
-#else
         __syncthreads();  // every warp is done reading stage s
         if (tid == 0 && t + kStages < ntile) {
             mbar_expect_tx(&full[s], kStageTx);
@@ -521,7 +475,6 @@ __global__ void __launch_bounds__(C::kThreads, kJerk ? C::kMinB : C::kMinBAcc) f
                 tma_load_1d(ring64 + s * kTile, a.pk64 + jc0 + (int64_t)(t + kStages) * kTile,
                             kT64TileBytes, &full[s]);
         }
-#endif
     }
 
     // chunk partial [chunk][kNC][n_loc_pad], coalesced fp64 stores
@@ -542,7 +495,6 @@ __global__ void __launch_bounds__(C::kThreads, kJerk ? C::kMinB : C::kMinBAcc) f
             for (int k = 0; k < kNC; ++k) out[(int64_t)k * a.n_loc_pad + il] = hacc[k][h];
         }
     }
-    }   // work item
 #undef ACC64
 }
 

@@ -15,11 +15,14 @@ sys.path.insert(0, ROOT)
 OUT = os.path.join(ROOT, "scripts", "sweep")
 
 VARIANTS = {
+    # the variants measured so far are recorded in profiles/r01_sweep_force.txt; the
+    # register-prefetch and per-warp empty-barrier ring experiments were removed from
+    # force.cu after measuring slower
     "base":      dict(),
-    "pf":        dict(FK_PREFETCH=1),
-    "pfu1":      dict(FK_PREFETCH=1, FK_UNROLL=1),
-    "pfu4":      dict(FK_PREFETCH=1, FK_UNROLL=4),
-    "pfst3":     dict(FK_PREFETCH=1, FK_STAGES=3),
+    "st3":       dict(FK_STAGES=3),
+    "b3u1":      dict(FK_MINB=3, FK_UNROLL=1),
+    "t64b4":     dict(FK_THREADS=64, FK_MINB=4),
+    "p3b3":      dict(FK_PAIRS=3, FK_MINB=3),
 }
 if os.environ.get("SWEEP_ONLY"):
     VARIANTS = {k: v for k, v in VARIANTS.items() if k in os.environ["SWEEP_ONLY"].split(",")}
