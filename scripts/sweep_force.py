@@ -23,6 +23,7 @@ VARIANTS = {
     "b3u1":      dict(FK_MINB=3, FK_UNROLL=1),
     "t64b4":     dict(FK_THREADS=64, FK_MINB=4),
     "p3b3":      dict(FK_PAIRS=3, FK_MINB=3),
+
 }
 if os.environ.get("SWEEP_ONLY"):
     VARIANTS = {k: v for k, v in VARIANTS.items() if k in os.environ["SWEEP_ONLY"].split(",")}
