@@ -599,7 +599,7 @@ bool use_small_cta(const ForceArgs& a) {
 
 cudaError_t launch_force(const ForceArgs& a, bool guard_self, bool jerk, cudaStream_t s) {
     if (a.c_count <= 0 || a.n_loc <= 0) return cudaSuccess;
-    if (a.ilist) return launch_cfg<CfgSmall>(a, guard_self, jerk, s);   // persistent list kernel
+    if (a.ilist) return launch_cfg<CfgSmall>(a, guard_self, jerk, s);   // active-list kernel
 #ifndef FK_NO_SMALL
     if (use_small_cta(a)) return launch_cfg<CfgSmall>(a, guard_self, jerk, s);
 #endif
