@@ -370,6 +370,8 @@ def main():
     sm_max = peaks.get("sm_max_mhz") or clk.get("sm_max_mhz") or 1965.0
     peak_tflops = sm_count * FP32_LANES_PER_SM * 2 * sm_max * 1e6 / 1e12
     n_loc = sim.n_loc
+    plan_info = binding.plan(n, world, rank)
+    plan_info["items"] = -(-n_loc // 1024) * plan_info["n_chunks"]
     force_launch_ms = force_ms / max(1, force_launches)
     i_evals_b = (act_b / world) if block else float(n_loc) * args.steps   # this rank's i per pass
     flops_per_launch = FLOPS_PER_INTERACTION * i_evals_b * float(n) / max(1, force_launches)
@@ -447,6 +449,9 @@ def main():
                 "l2": "flushed between steps (256 MiB memset outside the per-step events)"
                       if flush is not None else "not flushed",
                 "parallelism": f"i-shard x{world}",
+                "j_split": {k: plan_info[k] for k in ("chunk", "n_chunks")} | {
+                    "i_per_cta": 1024, "work_items_per_gpu": plan_info["items"],
+                    "note": "canonical (i-block x j-chunk) work items; results bit-identical for any P"},
                 **({"block_steps_per_step": block_steps_a / args.steps,
                     "mean_active": act_a / max(1, block_steps_a),
                     "force_evaluations_per_step": act_a / args.steps} if block else {}),
