@@ -510,7 +510,7 @@ template <bool G, bool J, bool H, class C>
 cudaError_t set_attr() {
     cudaError_t e = cudaFuncSetAttribute(force_kernel<G, J, H, C>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
-    if constexpr (J && std::is_same<C, CfgSmall>::value)   // persistent active-list variant
+    if constexpr (J && std::is_same<C, CfgSmall>::value)   // active-list variant (block steps)
         if (e == cudaSuccess)
             e = cudaFuncSetAttribute(force_kernel<G, J, H, C, true>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
