@@ -8,3 +8,4 @@ for spec in "C1 10" "C2 100" "C3 20" "C4 10" "C5 5" "PAPER 10"; do
 done
 timeout 900 python bench.py --config C4 --integrator leapfrog --steps 10 --warmup 3 --no-cpu-baseline 2>/dev/null | tail -1 >> gpurun_out/configs.jsonl
 timeout 900 python bench.py --config C5 --integrator leapfrog --steps 5 --warmup 3 --no-cpu-baseline 2>/dev/null | tail -1 >> gpurun_out/configs.jsonl
+timeout 900 python bench.py --config C4 --hilo on --steps 10 --warmup 3 --no-cpu-baseline 2>/dev/null | tail -1 >> gpurun_out/configs.jsonl
