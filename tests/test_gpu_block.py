@@ -255,3 +255,20 @@ def test_block_c3_schedule_and_state_vs_oracle():
     assert abs(sg[0] - so[0]) <= 0.01 * so[0] and abs(sg[1] - so[1]) <= 0.01 * so[1], (sg, so)
     assert np.max(np.abs(xg - xo)) <= 1e-9 and np.max(np.abs(vg - vo)) <= 2e-7, (
         np.max(np.abs(xg - xo)), np.max(np.abs(vg - vo)))
+
+
+def test_block_c2_long_run_energy_drift_vs_oracle():
+    """C2 (N = 16 384, eps = 1e-3) for 1/4 time unit of block steps (32 cycles of
+    dt_max = 1/128, ~4 500 block steps): the R#14 energy-drift rule against the oracle's own
+    block run, energies by the oracle's fp64 function."""
+    c = inputs.CONFIGS["C2"]
+    m, x, v = inputs.make("C2")
+    e2 = eps2_of(c.eps)
+    E0 = sum(oracle.energy(m, x, v, e2))
+    xg, vg, _, sg = run_block(m, x, v, c.eps, 1 / 128, 32)
+    xo, vo, _, _, _, so, _ = oracle.hermite_block(m, x, v, e2, 1 / 128, 32, eta=0.02, eta_s=0.01,
+                                                  kmax=20)
+    dg = abs(sum(oracle.energy(m, xg, vg, e2)) - E0) / abs(E0)
+    do = abs(sum(oracle.energy(m, xo, vo, e2)) - E0) / abs(E0)
+    assert dg <= 2 * max(do, 1e-11), (dg, do)
+    assert abs(sg[0] - so[0]) <= 0.02 * so[0], (sg, so)
