@@ -366,3 +366,22 @@ def test_get_state_partial_outputs_and_energy_consistency():
         ke1, pe1 = s.energy()
         ke2, pe2 = s.energy()
         assert (ke1, pe1) == (ke2, pe2)    # deterministic reduction
+
+
+@pytest.mark.parametrize("cfg", ["C4", "C5"])
+def test_full_size_properties_all_particles(cfg):
+    """Properties that hold at any size, checked on every particle of the full-size
+    configs in the bench's launch configuration (the oracle samples the rest): momentum
+    conservation (central pair forces, Sigma m a = 0) and permutation equivariance (a
+    seeded permutation of the particles permutes the forces; the j order changes, so
+    agreement is to fp32 rounding, not bitwise)."""
+    c = inputs.CONFIGS[cfg]
+    m, x, v = inputs.make(cfg)
+    a, j = gpu_forces(m, x, v, c.eps)
+    assert momentum_residual(m, a) < 1e-6, momentum_residual(m, a)
+    assert momentum_residual(m, j) < 1e-5, momentum_residual(m, j)
+    perm = np.random.default_rng(77).permutation(c.n)
+    ap, jp = gpu_forces(m[perm], x[:, perm], v[:, perm], c.eps)
+    assert max_rel(ap, a[:, perm]) <= 2 * TOL_ACC, max_rel(ap, a[:, perm])
+    assert max_rel(jp, j[:, perm]) <= 2 * TOL_JERK, max_rel(jp, j[:, perm])
+    assert paper_norm(ap, a[:, perm]) <= TOL_PAPER_ACC
