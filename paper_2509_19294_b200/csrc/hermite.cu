@@ -25,6 +25,8 @@
 
 #include <math.h>
 
+
+
 namespace nb {
 
 namespace {
@@ -273,74 +275,80 @@ __global__ void block_decide_kernel(long long* ctl, const unsigned long long* tn
 // results, every slot's force is the same j loop) and every local particle predicted to t_next with
 // its own polynomial (the predictor of predict() with dt -> D = t_next - t_i), packed for
 // the exchange.  In the block step past t_end the prediction is scratch nobody reads.
+// one particle of the active-set selection + prediction pass (append to *nact / ilist)
+__device__ __forceinline__ void select_predict_one(const StateArgs& a, int i, unsigned long long tn,
+                                                   double tick, int32_t* nact) {
+    if ((unsigned long long)(a.T[i] + ticks_of(a, a.lev[i])) == tn) {
+        const int slot = atomicAdd(nact, 1);
+        a.ilist[slot] = i;
+    }
+    const double D = (double)(int64_t)(tn - (unsigned long long)a.T[i]) * tick;
+    const double D2 = D * D, D3 = D2 * D;
+    double xp[3], vp[3];
+    bool ok = true;
+    for (int c = 0; c < 3; ++c) {
+        const int64_t o = c * a.n_loc_pad + i;
+        const double x = a.x[o], v = a.v[o], ac = a.a0[o], jk = a.j0[o];
+        xp[c] = x + v * D + ac * D2 / 2.0 + jk * D3 / 6.0;
+        vp[c] = v + ac * D + jk * D2 / 2.0;
+        a.xp[o] = xp[c];
+        a.vp[o] = vp[c];
+        ok = ok && isfinite(xp[c]) && isfinite(vp[c]);
+    }
+    if (!ok) flag_bad(a.bad, a.i_base + i);
+    store_packet(a, a.i_base + i, xp, vp, a.G * a.m[i]);
+}
+
 __global__ void block_select_predict_kernel(StateArgs a) {
     const unsigned long long tn = *a.tnext;
     const double tick = ldexp(a.dt, -a.kmax);
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < a.n_loc; i += gridDim.x * blockDim.x) {
-        if ((unsigned long long)(a.T[i] + ticks_of(a, a.lev[i])) == tn) {
-            const int slot = atomicAdd(a.nact, 1);
-            a.ilist[slot] = i;
-        }
-        const double D = (double)(int64_t)(tn - (unsigned long long)a.T[i]) * tick;
-        const double D2 = D * D, D3 = D2 * D;
-        double xp[3], vp[3];
-        bool ok = true;
-        for (int c = 0; c < 3; ++c) {
-            const int64_t o = c * a.n_loc_pad + i;
-            const double x = a.x[o], v = a.v[o], ac = a.a0[o], jk = a.j0[o];
-            xp[c] = x + v * D + ac * D2 / 2.0 + jk * D3 / 6.0;
-            vp[c] = v + ac * D + jk * D2 / 2.0;
-            a.xp[o] = xp[c];
-            a.vp[o] = vp[c];
-            ok = ok && isfinite(xp[c]) && isfinite(vp[c]);
-        }
-        if (!ok) flag_bad(a.bad, a.i_base + i);
-        store_packet(a, a.i_base + i, xp, vp, a.G * a.m[i]);
-    }
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < a.n_loc; i += gridDim.x * blockDim.x)
+        select_predict_one(a, i, tn, tick, a.nact);
 }
 
-// fold the active slots' chunk partials, Hermite corrector with the particle's
-// own dt_i (R#3 form), Aarseth criterion from a1, j1 and the interpolated
-// a^(2)(t_next) = a2 + dt a3, a^(3) = a3, block rules for the next level
+// one active slot of the corrector: fold, Hermite corrector with dt_i, Aarseth level
+__device__ __forceinline__ void correct_one(const StateArgs& a, int q, unsigned long long tn) {
+    const int i = a.ilist[q];
+    const int k = a.lev[i];
+    const double dt = dt_of(a, k);
+    const double dt2 = dt * dt, dt3 = dt2 * dt, dt4 = dt3 * dt, dt5 = dt4 * dt;
+    double s_a1 = 0, s_j1 = 0, s_a2 = 0, s_a3 = 0;
+    bool ok = true;
+    for (int c = 0; c < 3; ++c) {
+        const int64_t o = c * a.n_loc_pad + i;
+        const double a1 = fold(a, c, q), j1 = fold(a, 3 + c, q);
+        const double a0 = a.a0[o], j0 = a.j0[o];
+        const double a2 = (-6.0 * (a0 - a1) - dt * (4.0 * j0 + 2.0 * j1)) / dt2;
+        const double a3 = (12.0 * (a0 - a1) + 6.0 * dt * (j0 + j1)) / dt3;
+        const double x = a.xp[o] + a2 * dt4 / 24.0 + a3 * dt5 / 120.0;
+        const double v = a.vp[o] + a2 * dt3 / 6.0 + a3 * dt4 / 24.0;
+        a.x[o] = x;
+        a.v[o] = v;
+        a.a0[o] = a1;
+        a.j0[o] = j1;
+        const double a2t = a2 + dt * a3;
+        s_a1 += a1 * a1; s_j1 += j1 * j1; s_a2 += a2t * a2t; s_a3 += a3 * a3;
+        ok = ok && isfinite(x) && isfinite(v) && isfinite(a1) && isfinite(j1);
+    }
+    if (!ok) flag_bad(a.bad, a.i_base + i);
+    const double na1 = sqrt(s_a1), nj1 = sqrt(s_j1), na2 = sqrt(s_a2), na3 = sqrt(s_a3);
+    const double den = nj1 * na3 + na2 * na2;
+    const double dtc = den > 0.0 ? sqrt(a.eta * (na1 * na2 + nj1 * nj1) / den) : INFINITY;
+    int kn = k;
+    if (dtc < dt) {
+        while (kn < a.kmax && dt_of(a, kn) > dtc) ++kn;
+    } else if (k > 0 && dtc >= 2.0 * dt && tn % (2ull * (unsigned long long)ticks_of(a, k)) == 0) {
+        kn = k - 1;
+    }
+    a.lev[i] = kn;
+    a.T[i] = (int64_t)tn;
+}
+
 __global__ void block_correct_kernel(StateArgs a, int32_t* reset_nact, int reset_n, int32_t* done_ctas) {
     const int32_t n_act = *a.nact;
     const unsigned long long tn = *a.tnext;
-    for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n_act; q += gridDim.x * blockDim.x) {
-        const int i = a.ilist[q];
-        const int k = a.lev[i];
-        const double dt = dt_of(a, k);
-        const double dt2 = dt * dt, dt3 = dt2 * dt, dt4 = dt3 * dt, dt5 = dt4 * dt;
-        double s_a1 = 0, s_j1 = 0, s_a2 = 0, s_a3 = 0;
-        bool ok = true;
-        for (int c = 0; c < 3; ++c) {
-            const int64_t o = c * a.n_loc_pad + i;
-            const double a1 = fold(a, c, q), j1 = fold(a, 3 + c, q);
-            const double a0 = a.a0[o], j0 = a.j0[o];
-            const double a2 = (-6.0 * (a0 - a1) - dt * (4.0 * j0 + 2.0 * j1)) / dt2;
-            const double a3 = (12.0 * (a0 - a1) + 6.0 * dt * (j0 + j1)) / dt3;
-            const double x = a.xp[o] + a2 * dt4 / 24.0 + a3 * dt5 / 120.0;
-            const double v = a.vp[o] + a2 * dt3 / 6.0 + a3 * dt4 / 24.0;
-            a.x[o] = x;
-            a.v[o] = v;
-            a.a0[o] = a1;
-            a.j0[o] = j1;
-            const double a2t = a2 + dt * a3;
-            s_a1 += a1 * a1; s_j1 += j1 * j1; s_a2 += a2t * a2t; s_a3 += a3 * a3;
-            ok = ok && isfinite(x) && isfinite(v) && isfinite(a1) && isfinite(j1);
-        }
-        if (!ok) flag_bad(a.bad, a.i_base + i);
-        const double na1 = sqrt(s_a1), nj1 = sqrt(s_j1), na2 = sqrt(s_a2), na3 = sqrt(s_a3);
-        const double den = nj1 * na3 + na2 * na2;
-        const double dtc = den > 0.0 ? sqrt(a.eta * (na1 * na2 + nj1 * nj1) / den) : INFINITY;
-        int kn = k;
-        if (dtc < dt) {
-            while (kn < a.kmax && dt_of(a, kn) > dtc) ++kn;
-        } else if (k > 0 && dtc >= 2.0 * dt && tn % (2ull * (unsigned long long)ticks_of(a, k)) == 0) {
-            kn = k - 1;
-        }
-        a.lev[i] = kn;
-        a.T[i] = (int64_t)tn;
-    }
+    for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n_act; q += gridDim.x * blockDim.x)
+        correct_one(a, q, tn);
     // the last CTA of the last shard's launch resets t_next and the active counts for the
     // next block step (every CTA has read them by the time it counts itself done)
     if (reset_nact) {
@@ -356,6 +364,7 @@ __global__ void block_correct_kernel(StateArgs a, int32_t* reset_nact, int reset
         }
     }
 }
+
 
 unsigned grid_for(int64_t n) {
     int64_t g = (n + kBlock - 1) / kBlock;

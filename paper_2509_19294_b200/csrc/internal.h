@@ -154,6 +154,7 @@ struct BlockGraphNodes {
 cudaError_t launch_block_decide(long long* ctl, const unsigned long long* tnext, int32_t* nact,
                                 int nshards, cudaGraphConditionalHandle cond,
                                 const BlockGraphNodes* nodes, cudaStream_t s);
+
 // active set + every particle predicted to t_next and packed (one pass)
 cudaError_t launch_block_select_predict(const StateArgs& a, cudaStream_t s);
 // correct the active particles (count read on the device), new levels, T = t_next; with

@@ -272,3 +272,19 @@ def test_block_c2_long_run_energy_drift_vs_oracle():
     do = abs(sum(oracle.energy(m, xo, vo, e2)) - E0) / abs(E0)
     assert dg <= 2 * max(do, 1e-11), (dg, do)
     assert abs(sg[0] - so[0]) <= 0.02 * so[0], (sg, so)
+
+
+def test_block_execution_paths_bit_identical(monkeypatch):
+    """The two ways a block run executes -- one CUDA graph with a WHILE node (default) and
+    the host-driven loop (NBODY_NO_GRAPH=1, as with NCCL ranks or kernel timing) -- launch
+    the same kernels and give bit-identical states, levels and statistics."""
+    m, x, v = inputs.parity_round(*inputs.plummer(6000, 23))
+    out = []
+    for env in ({}, {"NBODY_NO_GRAPH": "1"}):
+        monkeypatch.delenv("NBODY_NO_GRAPH", raising=False)
+        for k, val in env.items():
+            monkeypatch.setenv(k, val)
+        out.append(run_block(m, x, v, 1e-3, 1 / 128, 3, world=2, loopback=True))
+    for o in out[1:]:
+        assert np.array_equal(o[0], out[0][0]) and np.array_equal(o[1], out[0][1])
+        assert np.array_equal(o[2], out[0][2]) and o[3] == out[0][3]
