@@ -131,3 +131,34 @@ def test_product_does_not_import_oracle():
                 src = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in src and "from oracle" not in src, f
                 assert "liboracle" not in src and "oracle_forces" not in src, f
+
+
+def _build_c_demo(tmp_path):
+    import subprocess
+    exe = tmp_path / "c_api_demo"
+    lib_dir = os.path.join(ROOT, "paper_2509_19294_b200")
+    binding.lib()   # builds libnbody.so if missing
+    subprocess.run(["gcc", "-O2", "-Wall", "-Werror", "-I", os.path.join(ROOT, "include"), "-o", str(exe),
+                    os.path.join(ROOT, "examples", "c_api_demo.c"), "-L", lib_dir, "-lnbody",
+                    f"-Wl,-rpath,{lib_dir}", "-lm"], check=True)
+    return exe
+
+
+def test_c_program_links_against_the_c_abi(tmp_path):
+    """examples/c_api_demo.c compiles against include/nbody.h and links libnbody.so with a
+    plain C compiler (no C++, no torch); the host-only nbody_plan runs without a GPU."""
+    import subprocess
+    exe = _build_c_demo(tmp_path)
+    out = subprocess.run([str(exe), "1000", "plan"], capture_output=True, text=True, check=True).stdout
+    assert "chunk=256 n_chunks=4" in out
+
+
+@pytest.mark.gpu
+def test_c_program_runs_the_hot_path(tmp_path):
+    """The same C program on the GPU: forces into host arrays, 10 Hermite steps, energy."""
+    import re
+    import subprocess
+    exe = _build_c_demo(tmp_path)
+    out = subprocess.run([str(exe), "4096"], capture_output=True, text=True, check=True).stdout
+    rel = float(re.search(r"rel\. change ([0-9.e+-]+)", out).group(1))
+    assert rel < 1e-6, out
