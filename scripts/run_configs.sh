@@ -9,3 +9,6 @@ done
 timeout 900 python bench.py --config C4 --integrator leapfrog --steps 10 --warmup 3 --no-cpu-baseline 2>/dev/null | tail -1 >> gpurun_out/configs.jsonl
 timeout 900 python bench.py --config C5 --integrator leapfrog --steps 5 --warmup 3 --no-cpu-baseline 2>/dev/null | tail -1 >> gpurun_out/configs.jsonl
 timeout 900 python bench.py --config C4 --hilo on --steps 10 --warmup 3 --no-cpu-baseline 2>/dev/null | tail -1 >> gpurun_out/configs.jsonl
+# block time steps (R#28) and the loopback scaling projection
+bash scripts/gpu_block_bench.sh
+timeout 1500 python scripts/project_scaling.py --configs C3,C4,C5 --steps 2 > gpurun_out/scaling_proj.jsonl 2> gpurun_out/scaling_proj.err
