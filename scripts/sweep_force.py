@@ -23,6 +23,9 @@ VARIANTS = {
     "b3u1":      dict(FK_MINB=3, FK_UNROLL=1),
     "t64b4":     dict(FK_THREADS=64, FK_MINB=4),
     "p3b3":      dict(FK_PAIRS=3, FK_MINB=3),
+    "b1":        dict(FK_MINB=1),
+    "b1u3":      dict(FK_MINB=1, FK_UNROLL=3),
+    "b1u4":      dict(FK_MINB=1, FK_UNROLL=4),
 
 }
 if os.environ.get("SWEEP_ONLY"):
