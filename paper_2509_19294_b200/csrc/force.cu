@@ -27,6 +27,8 @@
 #include "internal.h"
 
 #include <algorithm>
+#include <atomic>
+#include <mutex>
 #include <cstdlib>
 #include <cstring>
 #include <cstdio>
@@ -532,12 +534,21 @@ cudaError_t set_attrs() {
 }
 
 // dynamic shared memory above 48 KiB must be opted into once per instantiation
+// (a function attribute belongs to the current device's context: once per device)
 cudaError_t ensure_attrs() {
-    static cudaError_t done = [] {
-        cudaError_t e = set_attrs<CfgBig>(), r = set_attrs<CfgSmall>();
-        return e != cudaSuccess ? e : r;
-    }();
-    return done;
+    static std::mutex mu;
+    static std::atomic<uint64_t> done_mask{0};
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    const uint64_t bit = 1ull << (dev & 63);
+    if (done_mask.load(std::memory_order_acquire) & bit) return cudaSuccess;
+    std::lock_guard<std::mutex> lock(mu);
+    if (done_mask.load(std::memory_order_relaxed) & bit) return cudaSuccess;
+    e = set_attrs<CfgBig>();
+    if (e == cudaSuccess) e = set_attrs<CfgSmall>();
+    if (e == cudaSuccess) done_mask.fetch_or(bit, std::memory_order_release);
+    return e;
 }
 
 template <bool G, bool J, bool H, class C>
