@@ -221,7 +221,10 @@ __global__ void __launch_bounds__(C::kThreads, kJerk ? C::kMinB : C::kMinBAcc) f
             const int il = ib + (2 * p + h) * kThreads + tid;
             if (il < n_loc) {
                 int64_t src = a.i_base + il;
-                if constexpr (kList) src = a.i_base + a.ilist[il];   // block steps: active slot
+                if constexpr (kList) {   // block steps: active slot
+                    NB_CHECK(a.ilist[il] >= 0 && a.ilist[il] < a.n_loc);
+                    src = a.i_base + a.ilist[il];
+                }
                 const JPkt pk = a.pkt[src];
                 const float4 P = jpkt_pos(pk), V = jpkt_vel(pk);
                 q[h][0] = -P.x; q[h][1] = -P.y; q[h][2] = -P.z;
@@ -480,6 +483,8 @@ __global__ void __launch_bounds__(C::kThreads, kJerk ? C::kMinB : C::kMinBAcc) f
     }
 
     // chunk partial [chunk][kNC][n_loc_pad], coalesced fp64 stores
+    NB_CHECK(c >= 0 && c < a.n_chunks && jc0 + a.chunk <= (int64_t)a.n_chunks * a.chunk);
+    NB_CHECK(ib + kIPerBlock <= a.n_loc_pad || n_loc <= ib);
     double* out = a.partial + (int64_t)c * kNC * a.n_loc_pad;
 #pragma unroll
     for (int l = 0; l < 2 * kPairs; ++l) {

@@ -280,6 +280,7 @@ __device__ __forceinline__ void select_predict_one(const StateArgs& a, int i, un
                                                    double tick, int32_t* nact) {
     if ((unsigned long long)(a.T[i] + ticks_of(a, a.lev[i])) == tn) {
         const int slot = atomicAdd(nact, 1);
+        NB_CHECK(slot >= 0 && slot < a.n_loc);
         a.ilist[slot] = i;
     }
     const double D = (double)(int64_t)(tn - (unsigned long long)a.T[i]) * tick;
@@ -309,7 +310,9 @@ __global__ void block_select_predict_kernel(StateArgs a) {
 // one active slot of the corrector: fold, Hermite corrector with dt_i, Aarseth level
 __device__ __forceinline__ void correct_one(const StateArgs& a, int q, unsigned long long tn) {
     const int i = a.ilist[q];
+    NB_CHECK(q < a.n_loc && i >= 0 && i < a.n_loc);
     const int k = a.lev[i];
+    NB_CHECK(k >= 0 && k <= a.kmax && a.T[i] >= 0);
     const double dt = dt_of(a, k);
     const double dt2 = dt * dt, dt3 = dt2 * dt, dt4 = dt3 * dt, dt5 = dt4 * dt;
     double s_a1 = 0, s_j1 = 0, s_a2 = 0, s_a3 = 0;

@@ -4,6 +4,19 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+// NB_DEBUG_CHECKS=1 (debug builds only; tests/test_gpu_debug_checks.py): device-side bounds
+// asserts on every index the block-step and force kernels derive from device data.  The
+// pool this was built on has no compute-sanitizer, so these stand in for memcheck.
+#ifndef NB_DEBUG_CHECKS
+#define NB_DEBUG_CHECKS 0
+#endif
+#if NB_DEBUG_CHECKS
+#include <cassert>
+#define NB_CHECK(cond) assert(cond)
+#else
+#define NB_CHECK(cond) ((void)0)
+#endif
+
 namespace nb {
 
 // j-particle packet, the B200 replacement of the paper's replicated 32x32

@@ -1,7 +1,9 @@
 #!/usr/bin/env python
 """Small end-to-end case for compute-sanitizer (racecheck / memcheck / synccheck):
 every force-kernel instantiation (eps > 0 and eps = 0 guard, Hermite and
-leapfrog, hi/lo), loopback shards, graph replay and the energy kernel, N = 3000."""
+leapfrog, hi/lo, block-step active lists), loopback shards, graph replay and the
+energy kernel, N = 3000.  Also run against the NB_DEBUG_CHECKS=1 library
+(tests/test_gpu_debug_checks.py)."""
 import os
 import sys
 
@@ -14,7 +16,9 @@ from paper_2509_19294_b200 import binding, inputs  # noqa: E402
 m, x, v = inputs.parity_round(*inputs.plummer(3000, 3))
 st = torch.cuda.Stream()
 for kw in (dict(), dict(integrator="leapfrog"), dict(hilo=True), dict(world=3, loopback=True),
-           dict(eps=0.0), dict(eps=0.0, integrator="leapfrog", hilo=True)):
+           dict(eps=0.0), dict(eps=0.0, integrator="leapfrog", hilo=True),
+           dict(integrator="block"), dict(integrator="block", world=3, loopback=True),
+           dict(integrator="block", eps=0.0)):
     eps = kw.pop("eps", 1e-3)
     with binding.NBody(m, x, v, eps=eps, dt=1 / 1024, stream=st, **kw) as s:
         s.forces()
