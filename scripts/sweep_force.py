@@ -23,6 +23,8 @@ VARIANTS = {
     "b3u1":      dict(FK_MINB=3, FK_UNROLL=1),
     "t64b4":     dict(FK_THREADS=64, FK_MINB=4),
     "p3b3":      dict(FK_PAIRS=3, FK_MINB=3),
+    "t160":      dict(FK_THREADS=160),              # 10 warps per SM (3/3/2/2 per SMSP)
+    "t96b3":     dict(FK_THREADS=96, FK_MINB=3),   # 9 warps per SM
     "b1":        dict(FK_MINB=1),
     "b1u3":      dict(FK_MINB=1, FK_UNROLL=3),
     "b1u4":      dict(FK_MINB=1, FK_UNROLL=4),
