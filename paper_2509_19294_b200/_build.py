@@ -62,16 +62,17 @@ def nvcc() -> str:
     return p
 
 
-def build(force: bool = False, verbose: bool = False, defines=(), out: str | None = None) -> str:
+def build(force: bool = False, verbose: bool = False, defines=(), out: str | None = None,
+          extra_flags=()) -> str:
     """Compile every csrc/*.cu into one shared library (default: the in-tree LIB).
 
-    `defines` (e.g. ["FK_PAIRS=3"]) and `out` build tuning variants elsewhere
-    (scripts/sweep_force.py); the product library is always the default."""
+    `defines` (e.g. ["FK_PAIRS=3"]), `extra_flags` and `out` build tuning variants
+    elsewhere (scripts/sweep_force.py); the product library is always the default."""
     target = out or LIB
-    if not force and not defines and out is None and not stale():
+    if not force and not defines and not extra_flags and out is None and not stale():
         return LIB
     tmp = target + f".tmp{os.getpid()}"
-    cmd = [nvcc(), *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-I", INCLUDE, "-I", CSRC,
+    cmd = [nvcc(), *NVCC_FLAGS, *extra_flags, *[f"-D{d}" for d in defines], "-I", INCLUDE, "-I", CSRC,
            "-I", nccl_include(), "-o", tmp, *sources(), "-ldl"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if verbose or r.returncode:

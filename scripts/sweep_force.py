@@ -25,6 +25,8 @@ VARIANTS = {
     "p3b3":      dict(FK_PAIRS=3, FK_MINB=3),
     "t160":      dict(FK_THREADS=160),              # 10 warps per SM (3/3/2/2 per SMSP)
     "t96b3":     dict(FK_THREADS=96, FK_MINB=3),   # 9 warps per SM
+    "ptxO1":     dict(_FLAGS=("-Xptxas", "-O1")),   # ptxas optimisation level (schedule)
+    "ptxO2":     dict(_FLAGS=("-Xptxas", "-O2")),
     "b1":        dict(FK_MINB=1),
     "b1u3":      dict(FK_MINB=1, FK_UNROLL=3),
     "b1u4":      dict(FK_MINB=1, FK_UNROLL=4),
@@ -43,7 +45,8 @@ def build():
         name, d = item
         path = os.path.join(OUT, f"lib_{name}.so")
         try:
-            _build.build(defines=[f"{k}={v}" for k, v in d.items()], out=path)
+            _build.build(defines=[f"{k}={v}" for k, v in d.items() if k != "_FLAGS"], out=path,
+                         extra_flags=d.get("_FLAGS", ()))
             r = subprocess.run(["cuobjdump", "-res-usage", path], capture_output=True, text=True).stdout
             regs = [ln for ln in r.splitlines() if "force_kernelILb0" in ln]
             return name, "ok", regs
