@@ -8,6 +8,8 @@ What the N > 1 GPU path does per rank, exercised without GPUs:
   * the in-place all-gather of equal `slot`-sized packet slices reassembles the
     global j array in global particle order (emulated with gloo all_gather);
   * per-rank forces on the own i-range (oracle) concatenate to the full evaluation;
+  * block time steps: per-rank minima of t_i + dt_i reduced with MIN give the global
+    t_next, and the ranks' active sets partition the global active set;
   * bench.py's timing reduction is a MAX over ranks.
 """
 import os
@@ -66,7 +68,19 @@ def _worker(rank, world, port, n, q):
             j_all = np.concatenate([g[3] for g in got], axis=1)
             af, jf = oracle.forces(m, x, v, 1e-6)
             assert np.array_equal(a_all, af) and np.array_equal(j_all, jf)
-        # 4) max-over-ranks timing reduction (bench.py)
+        # 4) block time steps (R#28): every rank's minimum of t_i + dt_i over its own range,
+        #    reduced with MIN across ranks (the ncclAllReduce of block_run), is the global
+        #    t_next, and the ranks' active sets partition the global one
+        lev, _ = oracle.block_init_levels(*oracle.forces(m, x, v, 1e-6), 1 / 64, 20, 0.01)
+        due = (1 << (20 - lev.astype(np.int64)))          # t_i = 0: next time of particle i
+        tmin = torch.tensor([int(due[i0:i1].min()) if i1 > i0 else 2**62], dtype=torch.int64)
+        dist.all_reduce(tmin, op=dist.ReduceOp.MIN)
+        assert int(tmin) == int(due.min())
+        mine = [int(i) for i in np.nonzero(due[i0:i1] == int(tmin))[0] + i0]
+        act = [None] * world
+        dist.all_gather_object(act, mine)
+        assert sorted(sum(act, [])) == [int(i) for i in np.nonzero(due == due.min())[0]]
+        # 5) max-over-ranks timing reduction (bench.py)
         t = torch.tensor([10.0 + rank, 1.0 * rank], dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         assert t.tolist() == [10.0 + world - 1, float(world - 1)]
