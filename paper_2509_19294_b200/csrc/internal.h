@@ -90,7 +90,7 @@ struct ForceArgs {
     const int32_t* ilist;  // block steps: local index of the particle in i-slot il, or nullptr
                            // (slot il is particle il); partial rows are indexed by slot
     const int32_t* n_dev;  // with ilist: the active count on the device (n_loc is then only an
-                           // upper bound sizing the persistent grid)
+                           // the grid bound: host count, or the graph node grid set by decide)
 };
 
 // Launches the force pass for chunks c_first .. c_first + c_count - 1 (mod

@@ -651,7 +651,7 @@ namespace {
 // Block time steps (R#28): nsteps * dt_max of individual Hermite steps.  One block
 // step: reset counters, t_next = min(t_i + dt_i) (device reduction, NCCL min over
 // ranks), active lists, decide (done = t_next > t_end; statistics), predict + pack
-// everything, exchange, persistent force pass over the active slots (device count),
+// everything, exchange, force pass over the active slots (count read on the device),
 // correct + new levels.  No launch needs a host-side count, so without NCCL the whole
 // loop is one CUDA graph with a WHILE node whose condition the decide kernel sets;
 // with NCCL (or kernel timing on) the host drives the loop and reads `done`.
