@@ -89,8 +89,8 @@ struct ForceArgs {
     unsigned long long* coincident;  // eps == 0 only: min global i of a coincident pair
     const int32_t* ilist;  // block steps: local index of the particle in i-slot il, or nullptr
                            // (slot il is particle il); partial rows are indexed by slot
-    const int32_t* n_dev;  // with ilist: the active count on the device (n_loc is then only an
-                           // the grid bound: host count, or the graph node grid set by decide)
+    const int32_t* n_dev;  // with ilist: the active count on the device; n_loc then only sizes
+                           // the grid (host count, or a placeholder the decide kernel rewrites)
 };
 
 // Launches the force pass for chunks c_first .. c_first + c_count - 1 (mod
