@@ -106,21 +106,39 @@ __global__ void predict_pack_kernel(StateArgs a) {
     }
 }
 
-// canonical fold: ascending chunk order, fp64 left fold from +0
-__device__ __forceinline__ double fold(const StateArgs& a, int k, int i) {
-    if (k >= a.ncomp) return 0.0;   // leapfrog: no jerk
-    double s = 0.0;
-    const double* p = a.partial + (int64_t)k * a.n_loc_pad + i;
-    const int64_t stride = (int64_t)a.ncomp * a.n_loc_pad;
-    for (int c = 0; c < a.n_chunks; ++c) s += p[c * stride];
-    return s;
+
+// canonical fold of column i of the chunk partials: per component an ascending-chunk fp64
+// left fold from +0 (the order every path shares), all ncomp components at once with the components' loads interleaved so that 4 chunks x ncomp
+// independent loads are in flight (the fold is load-latency bound when few columns are
+// folded, e.g. a small block-step active set)
+__device__ __forceinline__ void fold_all(const StateArgs& a, int i, double out[6]) {
+    const double* p = a.partial + i;
+    const int64_t row = a.n_loc_pad, stride = (int64_t)a.ncomp * a.n_loc_pad;
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0, s4 = 0.0, s5 = 0.0;
+    if (a.ncomp == 6) {
+#pragma unroll 4
+        for (int c = 0; c < a.n_chunks; ++c) {
+            const double* q = p + c * stride;
+            s0 += q[0]; s1 += q[row]; s2 += q[2 * row];
+            s3 += q[3 * row]; s4 += q[4 * row]; s5 += q[5 * row];
+        }
+    } else {
+#pragma unroll 4
+        for (int c = 0; c < a.n_chunks; ++c) {
+            const double* q = p + c * stride;
+            s0 += q[0]; s1 += q[row]; s2 += q[2 * row];
+        }
+    }
+    out[0] = s0; out[1] = s1; out[2] = s2; out[3] = s3; out[4] = s4; out[5] = s5;
 }
 
 __global__ void fold_forces_kernel(StateArgs a) {
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < a.n_loc; i += gridDim.x * blockDim.x) {
         bool ok = true;
+        double f[6];
+        fold_all(a, i, f);
         for (int c = 0; c < 3; ++c) {
-            const double ac = fold(a, c, i), jk = fold(a, 3 + c, i);
+            const double ac = f[c], jk = f[3 + c];
             a.a0[c * a.n_loc_pad + i] = ac;
             a.j0[c * a.n_loc_pad + i] = jk;
             ok = ok && isfinite(ac) && isfinite(jk);
@@ -132,12 +150,13 @@ __global__ void fold_forces_kernel(StateArgs a) {
 __global__ void correct_predict_pack_kernel(StateArgs a) {
     const double dt = a.dt, dt2 = dt * dt, dt3 = dt2 * dt, dt4 = dt3 * dt, dt5 = dt4 * dt;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < a.n_loc; i += gridDim.x * blockDim.x) {
-        double x[3], v[3], a1[3], j1[3];
+        double x[3], v[3], a1[3], j1[3], f[6];
         bool ok = true;
+        fold_all(a, i, f);
         for (int c = 0; c < 3; ++c) {
             const int64_t o = c * a.n_loc_pad + i;
-            a1[c] = fold(a, c, i);
-            j1[c] = fold(a, 3 + c, i);
+            a1[c] = f[c];
+            j1[c] = f[3 + c];
             if (a.integrator == 0) {   // Hermite corrector (R#3)
                 const double a0 = a.a0[o], j0 = a.j0[o];
                 const double a2 = (-6.0 * (a0 - a1[c]) - dt * (4.0 * j0 + 2.0 * j1[c])) / dt2;
@@ -315,11 +334,12 @@ __device__ __forceinline__ void correct_one(const StateArgs& a, int q, unsigned 
     NB_CHECK(k >= 0 && k <= a.kmax && a.T[i] >= 0);
     const double dt = dt_of(a, k);
     const double dt2 = dt * dt, dt3 = dt2 * dt, dt4 = dt3 * dt, dt5 = dt4 * dt;
-    double s_a1 = 0, s_j1 = 0, s_a2 = 0, s_a3 = 0;
+    double s_a1 = 0, s_j1 = 0, s_a2 = 0, s_a3 = 0, f[6];
     bool ok = true;
+    fold_all(a, q, f);
     for (int c = 0; c < 3; ++c) {
         const int64_t o = c * a.n_loc_pad + i;
-        const double a1 = fold(a, c, q), j1 = fold(a, 3 + c, q);
+        const double a1 = f[c], j1 = f[3 + c];
         const double a0 = a.a0[o], j0 = a.j0[o];
         const double a2 = (-6.0 * (a0 - a1) - dt * (4.0 * j0 + 2.0 * j1)) / dt2;
         const double a3 = (12.0 * (a0 - a1) + 6.0 * dt * (j0 + j1)) / dt3;
