@@ -70,7 +70,8 @@ enum nbody_integrator {
 };
 
 typedef struct {
-    int64_t n;            /* total particles over all ranks, >= 2              */
+    int64_t n;            /* total particles over all ranks, >= 2; at most      
+                             2^31 - 1 per shard (n / world, rounded up)        */
     double G;             /* gravitational constant, finite, > 0               */
     double eps;           /* Plummer softening, finite, >= 0 (R#1).  The force
                              kernel uses eps2 = fp32(eps*eps) (R#18).  eps == 0
@@ -114,13 +115,14 @@ typedef struct {
 
 /* Partition and reduction plan (pure host function, no GPU needed).
  * Rank r owns the contiguous global range [i0, i1) with
- * i0 = r * slot, i1 = min(n, (r + 1) * slot), slot = 256 * ceil(n / (256 world)),
+ * i0 = r * slot, i1 = min(n, (r + 1) * slot), slot = B * ceil(n / (B world)) with
+ * B = 1024, the force kernel's i-block,
  * so all ranks but the last own `slot` particles (SPEC S:96 partition,
  * read with padding at the tail only so the j order never depends on world).
  * chunk = 256 * ceil(n / (256 * jchunks)) j-particles per canonical
  * reduction chunk, n_chunks = ceil(n / chunk).  Any output pointer may be
  * NULL.  Returns NBODY_EINVAL for n < 2, world < 1, world > n, rank outside
- * [0, world) or jchunks < 0. */
+ * [0, world), jchunks < 0 or slot > 2^31 - 1. */
 int nbody_plan(int64_t n, int32_t world, int32_t rank, int32_t jchunks,
                int64_t* i0, int64_t* i1, int64_t* slot, int64_t* chunk,
                int64_t* n_chunks);

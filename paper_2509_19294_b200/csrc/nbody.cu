@@ -51,9 +51,8 @@ struct NcclApi {
     const char* (*GetErrorString)(ncclResult_t) = nullptr;
 };
 
-NcclApi& nccl() {
-    static NcclApi api;
-    if (api.tried) return api;
+NcclApi load_nccl() {
+    NcclApi api;
     api.tried = true;
     const char* path = getenv("NBODY_NCCL_LIB");
     void* h = dlopen(path && *path ? path : "libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
@@ -79,6 +78,13 @@ NcclApi& nccl() {
     return api;
 }
 
+// resolved once per process; the function-local static makes concurrent first
+// calls from several threads safe
+NcclApi& nccl() {
+    static NcclApi api = load_nccl();
+    return api;
+}
+
 // ------------------------------------------------------------------ plan
 
 struct Plan {
@@ -98,6 +104,10 @@ int make_plan(int64_t n, int32_t world, int32_t rank, int32_t jchunks, Plan* p, 
     p->slot = B * ((n + B * world - 1) / (B * world));
     p->i0 = std::min<int64_t>(n, rank * p->slot);
     p->i1 = std::min<int64_t>(n, (int64_t)(rank + 1) * p->slot);
+    if (p->slot > INT32_MAX) {   // per-shard counts are int32 on the device
+        *why = "n / world must not exceed 2^31 - 1 particles per shard";
+        return NBODY_EINVAL;
+    }
     p->chunk = T * ((n + T * jc - 1) / (T * jc));
     p->n_chunks = (n + p->chunk - 1) / p->chunk;
     return NBODY_OK;

@@ -76,7 +76,7 @@ def test_plan_partition_covers_all_particles(n, world):
     for a, b in zip(ranges, ranges[1:]):
         assert a["i1"] == b["i0"]
     p = ranges[0]
-    assert p["slot"] % 256 == 0 and p["slot"] * world >= n
+    assert p["slot"] == 1024 * -(-n // (1024 * world))   # smallest multiple of the i-block
     assert p["chunk"] % 256 == 0 and p["n_chunks"] <= 128
     assert (p["n_chunks"] - 1) * p["chunk"] < n <= p["n_chunks"] * p["chunk"]
     # chunking does not depend on world (bit-identity across P)
@@ -84,7 +84,8 @@ def test_plan_partition_covers_all_particles(n, world):
 
 
 def test_plan_rejects_bad_arguments():
-    for args in [(1, 1, 0), (10, 0, 0), (10, 11, 0), (10, 2, 2), (10, 2, -1)]:
+    for args in [(1, 1, 0), (10, 0, 0), (10, 11, 0), (10, 2, 2), (10, 2, -1),
+                 (2**31, 1, 0), (2**33, 2, 1)]:   # > 2^31 - 1 particles per shard
         with pytest.raises(binding.NBodyError) as e:
             binding.plan(*args)
         assert e.value.code == binding.NBODY_EINVAL
