@@ -143,6 +143,12 @@ def _ptr(a):
     raise TypeError(f"unsupported array type {type(a)}")
 
 
+def _want(a, shape, name):
+    """Shape check before a raw pointer crosses the C-ABI (which trusts sizes)."""
+    if a is not None and tuple(a.shape) != tuple(shape):
+        raise ValueError(f"{name} must have shape {tuple(shape)}, got {tuple(a.shape)}")
+
+
 class NBody:
     """One rank's (or, with loopback=True, all ranks') view of an N-body system.
 
@@ -167,7 +173,11 @@ class NBody:
             raw_stream = 1   # cudaStreamLegacy: torch's default stream, not "library-created"
         self._keep = []
         m, x, v = (self._prep(a) for a in (m, x, v))
+        if m.ndim != 1:
+            raise ValueError("m must be one-dimensional (n,)")
         n = int(m.shape[0])
+        _want(x, (3, n), "x")
+        _want(v, (3, n), "v")
         if hilo is None:
             # block time steps difference forces over dt^2..dt^3 for the Aarseth
             # criterion; fp32-rounded positions make it noisy (R#28), so
@@ -210,6 +220,8 @@ class NBody:
             acc = torch.empty((3, self.n_loc), dtype=torch.float64, device=self.device)
         if jerk is None:
             jerk = torch.empty((3, self.n_loc), dtype=torch.float64, device=self.device)
+        _want(acc, (3, self.n_loc), "acc")
+        _want(jerk, (3, self.n_loc), "jerk")
         self._c(lib().nbody_compute_forces(self._ctx, _ptr(acc), _ptr(jerk)))
         return acc, jerk
 
@@ -227,10 +239,15 @@ class NBody:
             x = torch.empty((3, self.n_loc), dtype=torch.float64, device=self.device)
         if v is None:
             v = torch.empty((3, self.n_loc), dtype=torch.float64, device=self.device)
+        _want(x, (3, self.n_loc), "x")
+        _want(v, (3, self.n_loc), "v")
         self._c(lib().nbody_get_state(self._ctx, _ptr(x), _ptr(v)))
         return x, v
 
     def set_state(self, x, v, keep_forces=False):
+        """Overwrite the local (3, n_loc) positions and/or velocities (None keeps them)."""
+        _want(x, (3, self.n_loc), "x")
+        _want(v, (3, self.n_loc), "v")
         self._c(lib().nbody_set_state(self._ctx, _ptr(x), _ptr(v), 1 if keep_forces else 0))
 
     def sync(self):

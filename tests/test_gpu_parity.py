@@ -357,6 +357,25 @@ def test_c_abi_argument_errors():
     L.nbody_destroy(None)   # no-op
 
 
+def test_binding_rejects_wrong_shapes_before_the_c_abi():
+    """The C-ABI trusts array sizes; the binding checks shapes before passing pointers."""
+    m, x, v = inputs.make("C1")
+    with pytest.raises(ValueError, match="x must have shape"):
+        binding.NBody(m, x[:, :512], v, eps=1e-2, dt=1 / 1024)
+    with pytest.raises(ValueError, match="m must be one-dimensional"):
+        binding.NBody(m[None, :], x, v, eps=1e-2, dt=1 / 1024)
+    with binding.NBody(m, x, v, eps=1e-2, dt=1 / 1024) as s:
+        with pytest.raises(ValueError, match="acc must have shape"):
+            s.forces(acc=np.empty((3, 100)))
+        with pytest.raises(ValueError, match="v must have shape"):
+            s.state(v=np.empty((1024, 3)))
+        with pytest.raises(ValueError, match="x must have shape"):
+            s.set_state(np.empty(3 * 1024), None)
+        a, _ = s.forces()   # still usable
+        ao, _ = oracle.forces(m, x, v, eps2_of(1e-2))
+        assert max_rel(a.cpu().numpy(), ao) <= TOL_ACC
+
+
 def test_get_state_partial_outputs_and_energy_consistency():
     m, x, v = inputs.make("C1")
     with binding.NBody(m, x, v, eps=1e-2, dt=1 / 1024) as s:
