@@ -222,6 +222,13 @@ int nbody_prof_read(nbody_ctx* ctx, double* force_ms, int64_t* force_launches,
  * (per-emulated-GPU) times can be read off (scripts/project_scaling.py). */
 int nbody_prof_launch_times(nbody_ctx* ctx, double* ms, int64_t cap, int64_t* count);
 
+/* Sizes of the same launches: i particles (the active count for block time
+ * steps, read on the host loop that profiling selects) and real (unpadded) j
+ * particles, so n_i[k] * n_j[k] is launch k's interaction count.  Host-only,
+ * does not block; writes min(count, cap) entries of each non-NULL array. */
+int nbody_prof_launch_sizes(nbody_ctx* ctx, int64_t* n_i, int64_t* n_j, int64_t cap,
+                            int64_t* count);
+
 /* Message for the last failure on ctx (or of the last failed nbody_init /
  * plan call when ctx is NULL).  Never NULL; valid until the next call. */
 const char* nbody_last_error(const nbody_ctx* ctx);

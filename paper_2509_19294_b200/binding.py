@@ -22,7 +22,7 @@ EXPORTS = (
     "nbody_plan", "nbody_nccl_unique_id", "nbody_init", "nbody_local_range",
     "nbody_compute_forces", "nbody_step", "nbody_energy", "nbody_get_state",
     "nbody_set_state", "nbody_sync", "nbody_prof_enable", "nbody_prof_read",
-    "nbody_prof_launch_times", "nbody_block_stats",
+    "nbody_prof_launch_times", "nbody_prof_launch_sizes", "nbody_block_stats",
     "nbody_last_error", "nbody_destroy",
 )
 
@@ -96,6 +96,7 @@ def lib():
         "nbody_prof_enable": ([p, i32], ctypes.c_int),
         "nbody_prof_read": ([p, Pd, P64, P64, i32], ctypes.c_int),
         "nbody_prof_launch_times": ([p, p, i64, P64], ctypes.c_int),
+        "nbody_prof_launch_sizes": ([p, p, p, i64, P64], ctypes.c_int),
         "nbody_block_stats": ([p, P64, P64, p], ctypes.c_int),
         "nbody_last_error": ([p], ctypes.c_char_p),
         "nbody_destroy": ([p], None),
@@ -269,6 +270,15 @@ class NBody:
         out = np.zeros(n.value)
         self._c(lib().nbody_prof_launch_times(self._ctx, out.ctypes.data, n.value, ctypes.byref(n)))
         return out
+
+    def prof_launch_sizes(self):
+        """(n_i, n_j) int64 arrays of the launches prof_launch_times() reports."""
+        n = ctypes.c_int64()
+        self._c(lib().nbody_prof_launch_sizes(self._ctx, None, None, 0, ctypes.byref(n)))
+        ni, nj = np.zeros(n.value, dtype=np.int64), np.zeros(n.value, dtype=np.int64)
+        self._c(lib().nbody_prof_launch_sizes(self._ctx, ni.ctypes.data, nj.ctypes.data, n.value,
+                                              ctypes.byref(n)))
+        return ni, nj
 
     def block_stats(self, levels=False):
         """Block time steps: (block steps, sum of active counts[, levels int32 (n_loc,)])."""

@@ -176,6 +176,141 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t
         : "memory");
 }
 
+// j operands of one interaction, broadcast to both lanes of a pair
+struct JOps {
+    f2 x, y, z, m, eps2, vx, vy, vz, lx, ly, lz;
+    float mass;   // G m_j (eps = 0 report: padding j has mass 0)
+};
+// negated i state of one packed i-pair
+struct IPair {
+    f2 nx, ny, nz, nvx, nvy, nvz, nlx, nly, nlz;
+};
+
+// j operands of tile entry jj (shared memory), broadcast to both pair lanes
+template <bool kJerk, bool kHiLo>
+__device__ __forceinline__ JOps load_jops(const JPkt* tile, const float4* tile_lo, int jj) {
+    JOps jo;
+#if NB_PKT_DUP
+    // j operands arrive as {v, v} register pairs (packet layout, internal.h)
+    const ulonglong2 A = *reinterpret_cast<const ulonglong2*>(&tile[jj].a);
+    const ulonglong2 B = *reinterpret_cast<const ulonglong2*>(&tile[jj].b);
+    const ulonglong2 D = *reinterpret_cast<const ulonglong2*>(&tile[jj].d);
+    jo.x = A.x; jo.y = A.y; jo.z = B.x; jo.m = B.y; jo.eps2 = D.y;
+    jo.vx = jo.vy = jo.vz = 0ull;
+    if (kJerk) {
+        const ulonglong2 Cc = *reinterpret_cast<const ulonglong2*>(&tile[jj].c);
+        jo.vx = Cc.x; jo.vy = Cc.y; jo.vz = D.x;
+    }
+    jo.mass = tile[jj].b.z;
+#else
+    const float4 P = tile[jj].p;
+    const float4 V = tile[jj].v;
+    jo.x = f2bc(P.x); jo.y = f2bc(P.y); jo.z = f2bc(P.z); jo.m = f2bc(P.w);
+    jo.eps2 = f2bc(V.w);
+    jo.vx = f2bc(V.x); jo.vy = f2bc(V.y); jo.vz = f2bc(V.z);
+    jo.mass = P.w;
+#endif
+    jo.lx = jo.ly = jo.lz = 0ull;
+    if (kHiLo) {
+        const float4 L = tile_lo[jj];
+        jo.lx = f2bc(L.x); jo.ly = f2bc(L.y); jo.lz = f2bc(L.z);
+    }
+    return jo;
+}
+
+// negated i state of the particle in packet src (0 for a padding slot)
+template <bool kHiLo>
+__device__ __forceinline__ void load_i(const ForceArgs& a, bool valid, int64_t src, float (&q)[9]) {
+    if (valid) {
+        const JPkt pk = a.pkt[src];
+        const float4 P = jpkt_pos(pk), V = jpkt_vel(pk);
+        q[0] = -P.x; q[1] = -P.y; q[2] = -P.z;
+        q[3] = -V.x; q[4] = -V.y; q[5] = -V.z;
+        if (kHiLo) {
+            const float4 Lo = a.pklo[src];
+            q[6] = -Lo.x; q[7] = -Lo.y; q[8] = -Lo.z;
+        } else {
+            q[6] = q[7] = q[8] = 0.f;
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < 9; ++k) q[k] = 0.f;
+    }
+}
+
+// eps = 0, s == 0 in i-slot sl: a coincident pair unless it is the self term
+// (same global index) or padding (slot past n_loc, or a massless padding j)
+struct GuardCtx {   // what the eps = 0 report needs (kernel parameters, passed by value)
+    const int32_t* ilist;
+    int64_t i_base;
+    unsigned long long* coincident;
+    int n_loc;
+};
+template <bool kList>
+__device__ __forceinline__ void report_coincident(const GuardCtx& g, int sl, int64_t jg, float jmass) {
+    if (sl >= g.n_loc || jmass == 0.f) return;
+    const int64_t ig = g.i_base + (kList ? g.ilist[sl] : sl);
+    if (ig != jg) atomicMin(g.coincident, (unsigned long long)ig);
+}
+
+// One j against one packed i-pair: the FP32 interaction of the file header,
+// accumulated into pair p's tile sums acc[0..kNC)[p]; m3 = {-3, -3}.  Every force kernel
+// (all CTA shapes, the tile-split active-list kernel) runs exactly this
+// instruction sequence per lane, so their tile sums are bit-identical.
+// kGuard (eps = 0): s == 0 gives ri = 0 and reports a coincident pair of
+// distinct particles; sl_lo / sl_hi are the lanes' i-slots.
+template <bool kGuard, bool kJerk, bool kHiLo, bool kList, int kNC, int kP>
+__device__ __forceinline__ void interact(const JOps& j, const IPair& i, f2 (&acc)[kNC][kP], int p,
+                                         f2 m3, int sl_lo, int sl_hi, int64_t jg, const GuardCtx& g) {
+    f2 dx = fadd2(j.x, i.nx);
+    f2 dy = fadd2(j.y, i.ny);
+    f2 dz = fadd2(j.z, i.nz);
+    if (kHiLo) {   // d = (x_j^hi - x_i^hi) + (x_j^lo - x_i^lo)   (NEXT f2)
+        dx = fadd2(dx, fadd2(j.lx, i.nlx));
+        dy = fadd2(dy, fadd2(j.ly, i.nly));
+        dz = fadd2(dz, fadd2(j.lz, i.nlz));
+    }
+    f2 s2 = ffma2(dx, dx, j.eps2);
+    s2 = ffma2(dy, dy, s2);
+    s2 = ffma2(dz, dz, s2);
+    float s_lo, s_hi;
+    f2split(s2, s_lo, s_hi);
+    float r_lo = rsqrt_ftz(s_lo), r_hi = rsqrt_ftz(s_hi);
+    if (kGuard) {  // eps == 0: exclude j == i (s == 0), R#17
+        if (s_lo == 0.f) {
+            r_lo = 0.f;
+            report_coincident<kList>(g, sl_lo, jg, j.mass);
+        }
+        if (s_hi == 0.f) {
+            r_hi = 0.f;
+            report_coincident<kList>(g, sl_hi, jg, j.mass);
+        }
+    }
+    const f2 ri = f2make(r_lo, r_hi);
+#if FK_RCP   // 1/s from MUFU.RCP (XU pipe) instead of ri * ri on the FMA pipe
+    f2 ri2 = f2make(rcp_ftz(s_lo), rcp_ftz(s_hi));
+    if (kGuard) ri2 = fmul2(ri, ri);
+#else
+    const f2 ri2 = fmul2(ri, ri);
+#endif
+    const f2 mr3 = fmul2(fmul2(j.m, ri), ri2);      // G m_j / s^{3/2}
+    acc[0][p] = ffma2(mr3, dx, acc[0][p]);
+    acc[1][p] = ffma2(mr3, dy, acc[1][p]);
+    acc[2][p] = ffma2(mr3, dz, acc[2][p]);
+    if (kJerk) {
+        const f2 wx = fadd2(j.vx, i.nvx);
+        const f2 wy = fadd2(j.vy, i.nvy);
+        const f2 wz = fadd2(j.vz, i.nvz);
+        f2 rv = fmul2(dx, wx);
+        rv = ffma2(dy, wy, rv);
+        rv = ffma2(dz, wz, rv);                     // d . w
+        const f2 q3 = fmul2(fmul2(rv, ri2), m3);    // -3 (d.w) / s
+        acc[3 % kNC][p] = ffma2(mr3, ffma2(q3, dx, wx), acc[3 % kNC][p]);
+        acc[4 % kNC][p] = ffma2(mr3, ffma2(q3, dy, wy), acc[4 % kNC][p]);
+        acc[5 % kNC][p] = ffma2(mr3, ffma2(q3, dz, wz), acc[5 % kNC][p]);
+    }
+}
+
 template <bool kGuard, bool kJerk, bool kHiLo, class C, bool kList = false>
 __global__ void __launch_bounds__(C::kThreads, kJerk ? C::kMinB : C::kMinBAcc) force_kernel(ForceArgs a) {
     constexpr int kPairs = C::kPairs, kThreads = C::kThreads, kHyb = C::kHyb;
@@ -298,7 +433,12 @@ __global__ void __launch_bounds__(C::kThreads, kJerk ? C::kMinB : C::kMinBAcc) f
         }
     }
 
+    const GuardCtx gc{a.ilist, a.i_base, a.coincident, n_loc};
     const f2 m3 = f2bc(-3.0f);
+    IPair ip[kPairs];
+#pragma unroll
+    for (int p = 0; p < kPairs; ++p)
+        ip[p] = IPair{nx[p], ny[p], nz[p], nvx[p], nvy[p], nvz[p], nlx[p], nly[p], nlz[p]};
 
     for (int t = 0; t < ntile; ++t) {
         const int s = t % kStages;
@@ -306,9 +446,6 @@ __global__ void __launch_bounds__(C::kThreads, kJerk ? C::kMinB : C::kMinBAcc) f
         const JPkt* tile = ring + s * kTile;
         const float4* tile_lo = ring_lo + s * kTile;
         const JPkt64* tile64 = ring64 + s * kTile;
-#if defined(FK_EXP_NOLDS) && !NB_PKT_DUP
-        float4 Pr = tile[0].p, Vr = tile[0].v;
-#endif
 
         f2 acc[kNC][kPairs];
 #pragma unroll
@@ -318,106 +455,12 @@ __global__ void __launch_bounds__(C::kThreads, kJerk ? C::kMinB : C::kMinBAcc) f
 
 #pragma unroll kUnroll
         for (int jj = 0; jj < kTile; ++jj) {
-#if NB_PKT_DUP
-            // j operands arrive as {v, v} register pairs (packet layout, internal.h)
-            const ulonglong2 A = *reinterpret_cast<const ulonglong2*>(&tile[jj].a);
-            const ulonglong2 B = *reinterpret_cast<const ulonglong2*>(&tile[jj].b);
-            const ulonglong2 D = *reinterpret_cast<const ulonglong2*>(&tile[jj].d);
-            const f2 xj = A.x, yj = A.y, zj = B.x, mj = B.y, eps2 = D.y;
-            f2 vxj = 0, vyj = 0, vzj = 0;
-            if (kJerk) {
-                const ulonglong2 C = *reinterpret_cast<const ulonglong2*>(&tile[jj].c);
-                vxj = C.x; vyj = C.y; vzj = D.x;
-            }
-            const float jmass = tile[jj].b.z;
-#else
-#ifdef FK_EXP_NOLDS   // timing experiment only: j data from registers, perturbed by ALU ops
-            Pr.x = __int_as_float(__float_as_int(Pr.x) + 1);
-            Pr.y = __int_as_float(__float_as_int(Pr.y) + 1);
-            Pr.z = __int_as_float(__float_as_int(Pr.z) + 1);
-            Pr.w = __int_as_float(__float_as_int(Pr.w) + 1);
-            Vr.x = __int_as_float(__float_as_int(Vr.x) + 1);
-            Vr.y = __int_as_float(__float_as_int(Vr.y) + 1);
-            Vr.z = __int_as_float(__float_as_int(Vr.z) + 1);
-            Vr.w = __int_as_float(__float_as_int(Vr.w) + 1);
-            const float4 P = Pr;
-            const float4 V = Vr;
-#else
-            const float4 P = tile[jj].p;
-            const float4 V = tile[jj].v;
-#endif
-            const f2 xj = f2bc(P.x), yj = f2bc(P.y), zj = f2bc(P.z), mj = f2bc(P.w);
-            const f2 eps2 = f2bc(V.w);
-            const f2 vxj = f2bc(V.x), vyj = f2bc(V.y), vzj = f2bc(V.z);
-            const float jmass = P.w;
-#endif
-            f2 lxj = 0ull, lyj = 0ull, lzj = 0ull;
-            if (kHiLo) {
-                const float4 L = tile_lo[jj];
-                lxj = f2bc(L.x); lyj = f2bc(L.y); lzj = f2bc(L.z);
-            }
+            const JOps jo = load_jops<kJerk, kHiLo>(tile, tile_lo, jj);
+            const int64_t jg = kGuard ? jc0 + (int64_t)t * kTile + jj : 0;
 #pragma unroll
-            for (int p = 0; p < kPairs; ++p) {
-                f2 dx = fadd2(xj, nx[p]);
-                f2 dy = fadd2(yj, ny[p]);
-                f2 dz = fadd2(zj, nz[p]);
-                if (kHiLo) {   // d = (x_j^hi - x_i^hi) + (x_j^lo - x_i^lo)   (NEXT f2)
-                    dx = fadd2(dx, fadd2(lxj, nlx[p]));
-                    dy = fadd2(dy, fadd2(lyj, nly[p]));
-                    dz = fadd2(dz, fadd2(lzj, nlz[p]));
-                }
-                f2 s2 = ffma2(dx, dx, eps2);
-                s2 = ffma2(dy, dy, s2);
-                s2 = ffma2(dz, dz, s2);
-                float s_lo, s_hi;
-                f2split(s2, s_lo, s_hi);
-#ifdef FK_EXP_NOMUFU  // timing experiment only
-                float r_lo = s_lo, r_hi = s_hi;
-                asm volatile("" : "+f"(r_lo), "+f"(r_hi));
-#else
-                float r_lo = rsqrt_ftz(s_lo), r_hi = rsqrt_ftz(s_hi);
-#endif
-                if (kGuard) {  // eps == 0: exclude j == i (s == 0), R#17
-                    const int64_t jg = jc0 + (int64_t)t * kTile + jj;
-                    if (s_lo == 0.f) {
-                        r_lo = 0.f;
-                        const int sl = ib + (2 * p) * kThreads + tid;
-                        const int64_t ig = a.i_base + (kList && sl < n_loc ? a.ilist[sl] : sl);
-                        if (ig != jg && sl < n_loc && jmass != 0.f)
-                            atomicMin(a.coincident, (unsigned long long)ig);
-                    }
-                    if (s_hi == 0.f) {
-                        r_hi = 0.f;
-                        const int sl = ib + (2 * p + 1) * kThreads + tid;
-                        const int64_t ig = a.i_base + (kList && sl < n_loc ? a.ilist[sl] : sl);
-                        if (ig != jg && sl < n_loc && jmass != 0.f)
-                            atomicMin(a.coincident, (unsigned long long)ig);
-                    }
-                }
-                const f2 ri = f2make(r_lo, r_hi);
-#if FK_RCP   // 1/s from MUFU.RCP (XU pipe) instead of ri * ri on the FMA pipe
-                f2 ri2 = f2make(rcp_ftz(s_lo), rcp_ftz(s_hi));
-                if (kGuard) ri2 = fmul2(ri, ri);
-#else
-                const f2 ri2 = fmul2(ri, ri);
-#endif
-                const f2 mr3 = fmul2(fmul2(mj, ri), ri2);      // G m_j / s^{3/2}
-                acc[0][p] = ffma2(mr3, dx, acc[0][p]);
-                acc[1][p] = ffma2(mr3, dy, acc[1][p]);
-                acc[2][p] = ffma2(mr3, dz, acc[2][p]);
-                if (kJerk) {
-                    const f2 wx = fadd2(vxj, nvx[p]);
-                    const f2 wy = fadd2(vyj, nvy[p]);
-                    const f2 wz = fadd2(vzj, nvz[p]);
-                    f2 rv = fmul2(dx, wx);
-                    rv = ffma2(dy, wy, rv);
-                    rv = ffma2(dz, wz, rv);                     // d . w
-                    const f2 q3 = fmul2(fmul2(rv, ri2), m3);    // -3 (d.w) / s
-                    acc[3 % kNC][p] = ffma2(mr3, ffma2(q3, dx, wx), acc[3 % kNC][p]);
-                    acc[4 % kNC][p] = ffma2(mr3, ffma2(q3, dy, wy), acc[4 % kNC][p]);
-                    acc[5 % kNC][p] = ffma2(mr3, ffma2(q3, dz, wz), acc[5 % kNC][p]);
-                }
-            }
+            for (int p = 0; p < kPairs; ++p)
+                interact<kGuard, kJerk, kHiLo, kList>(jo, ip[p], acc, p, m3, ib + 2 * p * kThreads + tid,
+                                                      ib + (2 * p + 1) * kThreads + tid, jg, gc);
             // ---- the same interaction in fp64 for the thread's kHyb fp64 i-particles.
             //      DADD/DFMA/DMUL issue to the FP64 pipe, which runs beside FFMA2
             //      (scripts/ubench_fp32.cu: 4 FFMA2 : 3 DFMA keeps ~95 % of the FP32 rate).
@@ -505,9 +548,115 @@ __global__ void __launch_bounds__(C::kThreads, kJerk ? C::kMinB : C::kMinBAcc) f
 #undef ACC64
 }
 
+// ---- tile-split active-list kernel (block time steps, small active sets).
+// The list kernel gives each CTA a whole chunk (chunk / 256 tiles) of j for
+// its i: with a few active particles the launch has only n_chunks CTAs of
+// one serial j loop each and leaves most of the GPU idle (scripts/
+// block_launch_sizes.py).  Here CTA = (64 active i, chunk) with one warp per
+// tile: every lane holds one packed i-pair (slots ib + lane, ib + 32 + lane),
+// warp w stages tile r0 + w into its own shared-memory buffer and computes
+// that tile's fp32 sums with interact(), and after each round of W tiles the
+// CTA adds the round's tile sums to the fp64 chunk sums in ascending tile
+// order -- the same additions, in the same order, as force_kernel, so the
+// partials are bit-identical to the list kernel's.
+constexpr int kTsWarpsMax = 8;
+constexpr int kTsplitMaxDefault = 1024;
+constexpr int kTsI = 64;
+constexpr int kTsNC = 6;
+template <bool kHiLo>
+struct TsCfg {
+    static constexpr int kTileB = kTileBytes + (kHiLo ? kLoTileBytes : 0);
+    static constexpr int kOffSum = kTsWarpsMax * kTileB;                       // [W][6][64] fp32
+    static constexpr int kOffAcc = kOffSum + kTsWarpsMax * kTsNC * kTsI * 4;   // [6][64] fp64
+    static constexpr int kSmemBytes = kOffAcc + kTsNC * kTsI * 8;
+};
+
+template <bool kGuard, bool kHiLo>
+__global__ void __launch_bounds__(kTsWarpsMax * 32, 2) force_tsplit_kernel(ForceArgs a) {
+    using C = TsCfg<kHiLo>;
+    const int n_loc = *a.n_dev;
+    const int ib = (int)blockIdx.x * kTsI;
+    if (ib >= n_loc) return;
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, W = (int)blockDim.x >> 5;
+    JPkt* tile = reinterpret_cast<JPkt*>(smem + w * C::kTileB);
+    float4* tile_lo = reinterpret_cast<float4*>(smem + w * C::kTileB + kTileBytes);
+    float* tsum = reinterpret_cast<float*>(smem + C::kOffSum);
+    double* acc64 = reinterpret_cast<double*>(smem + C::kOffAcc);
+
+    float q[2][9];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int il = ib + h * 32 + lane;
+        const bool valid = il < n_loc;
+        if (valid) NB_CHECK(a.ilist[il] >= 0 && a.ilist[il] < a.n_loc);
+        load_i<kHiLo>(a, valid, valid ? a.i_base + a.ilist[il] : 0, q[h]);
+    }
+    const IPair ip{f2make(q[0][0], q[1][0]), f2make(q[0][1], q[1][1]), f2make(q[0][2], q[1][2]),
+                   f2make(q[0][3], q[1][3]), f2make(q[0][4], q[1][4]), f2make(q[0][5], q[1][5]),
+                   f2make(q[0][6], q[1][6]), f2make(q[0][7], q[1][7]), f2make(q[0][8], q[1][8])};
+    const GuardCtx gc{a.ilist, a.i_base, a.coincident, n_loc};
+    const f2 m3 = f2bc(-3.0f);
+    for (int k = tid; k < kTsNC * kTsI; k += blockDim.x) acc64[k] = 0.0;
+
+    const int c = (a.c_first + (int)blockIdx.y) % a.n_chunks;
+    const int64_t jc0 = (int64_t)c * a.chunk;
+    const int ntile = a.chunk / kTile;
+    for (int r0 = 0; r0 < ntile; r0 += W) {
+        const int t = r0 + w;
+        if (t < ntile) {
+            // stage tile t (L2-resident packets), warp-cooperative 16-B loads
+            const uint4* src = reinterpret_cast<const uint4*>(a.pkt + jc0 + (int64_t)t * kTile);
+            uint4* dst = reinterpret_cast<uint4*>(tile);
+#pragma unroll 4
+            for (int k = lane; k < kTileBytes / 16; k += 32) dst[k] = __ldg(src + k);
+            if (kHiLo) {
+                const uint4* sl = reinterpret_cast<const uint4*>(a.pklo + jc0 + (int64_t)t * kTile);
+                uint4* dl = reinterpret_cast<uint4*>(tile_lo);
+#pragma unroll 4
+                for (int k = lane; k < kLoTileBytes / 16; k += 32) dl[k] = __ldg(sl + k);
+            }
+            __syncwarp();
+            f2 acc[kTsNC][1];
+#pragma unroll
+            for (int k = 0; k < kTsNC; ++k) acc[k][0] = 0ull;
+#pragma unroll kUnroll
+            for (int jj = 0; jj < kTile; ++jj) {
+                const JOps jo = load_jops<true, kHiLo>(tile, tile_lo, jj);
+                const int64_t jg = kGuard ? jc0 + (int64_t)t * kTile + jj : 0;
+                interact<kGuard, true, kHiLo, true>(jo, ip, acc, 0, m3, ib + lane, ib + 32 + lane, jg, gc);
+            }
+            float* ts = tsum + w * kTsNC * kTsI;
+#pragma unroll
+            for (int k = 0; k < kTsNC; ++k) {
+                float lo, hi;
+                f2split(acc[k][0], lo, hi);
+                ts[k * kTsI + lane] = lo;
+                ts[k * kTsI + 32 + lane] = hi;
+            }
+        }
+        __syncthreads();   // this round's tile sums are in shared memory
+        const int nr = min(W, ntile - r0);
+        for (int k = tid; k < kTsNC * kTsI; k += blockDim.x) {
+            double sum = acc64[k];
+            for (int u = 0; u < nr; ++u) sum += (double)tsum[u * kTsNC * kTsI + k];   // ascending tiles
+            acc64[k] = sum;
+        }
+        __syncthreads();   // tile buffers and tile sums are free for the next round
+    }
+    NB_CHECK(c >= 0 && c < a.n_chunks);
+    double* out = a.partial + (int64_t)c * kTsNC * a.n_loc_pad;
+    for (int k = tid; k < kTsNC * kTsI; k += blockDim.x) {
+        const int il = ib + k % kTsI;
+        if (il < n_loc) out[(int64_t)(k / kTsI) * a.n_loc_pad + il] = acc64[k];
+    }
+}
+
 }  // namespace
 
 int force_i_per_block() { return kIPerBlock; }
+int force_tsplit_i_per_block() { return kTsI; }
+int force_tsplit_threads(int chunk) { return 32 * std::max(1, std::min(kTsWarpsMax, chunk / kTile)); }
 int force_list_i_per_block() { return CfgSmall::kIPerBlock; }
 int force_hyb() { return kHyb; }
 
@@ -552,6 +701,18 @@ cudaError_t ensure_attrs() {
     if (done_mask.load(std::memory_order_relaxed) & bit) return cudaSuccess;
     e = set_attrs<CfgBig>();
     if (e == cudaSuccess) e = set_attrs<CfgSmall>();
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(force_tsplit_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 TsCfg<false>::kSmemBytes);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(force_tsplit_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 TsCfg<true>::kSmemBytes);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(force_tsplit_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 TsCfg<false>::kSmemBytes);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(force_tsplit_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 TsCfg<true>::kSmemBytes);
     if (e == cudaSuccess) done_mask.fetch_or(bit, std::memory_order_release);
     return e;
 }
@@ -620,6 +781,29 @@ cudaError_t launch_force(const ForceArgs& a, bool guard_self, bool jerk, cudaStr
     if (use_small_cta(a)) return launch_cfg<CfgSmall>(a, guard_self, jerk, s);
 #endif
     return launch_cfg<CfgBig>(a, guard_self, jerk, s);
+}
+
+template <bool G, bool H>
+cudaError_t launch_tsplit(const ForceArgs& a, cudaStream_t s) {
+    const dim3 grid((unsigned)std::max<int64_t>(1, (a.n_loc + kTsI - 1) / kTsI), (unsigned)a.c_count);
+    force_tsplit_kernel<G, H><<<grid, force_tsplit_threads(a.chunk), TsCfg<H>::kSmemBytes, s>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_force_tsplit(const ForceArgs& a, bool guard_self, cudaStream_t s) {
+    if (a.c_count <= 0 || a.n_loc <= 0) return cudaSuccess;
+    if (!a.ilist || !a.n_dev) return cudaErrorInvalidValue;   // active-list launches only
+    cudaError_t e = ensure_attrs();
+    if (e != cudaSuccess) return e;
+    if (guard_self) return a.pklo ? launch_tsplit<true, true>(a, s) : launch_tsplit<true, false>(a, s);
+    return a.pklo ? launch_tsplit<false, true>(a, s) : launch_tsplit<false, false>(a, s);
+}
+
+// Active counts up to this use the tile-split kernel when a chunk has >= 2 tiles
+// (NBODY_TSPLIT_MAX overrides; 0 disables).  Chosen by scripts/block_launch_sizes.py.
+int force_tsplit_max() {
+    const char* e = getenv("NBODY_TSPLIT_MAX");   // read per call: tests switch it per context
+    return e && *e ? std::max(0, atoi(e)) : kTsplitMaxDefault;
 }
 
 int force_ctas_per_sm(bool jerk, bool hilo) {

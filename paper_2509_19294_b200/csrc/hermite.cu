@@ -282,9 +282,17 @@ __global__ void block_decide_kernel(long long* ctl, const unsigned long long* tn
     if (nodes) {   // inside the block-step graph
         for (int q = 0; q < nshards; ++q) {
             if (!nodes->force[q]) continue;   // shard without particles: no force node
-            const int nb = (nact[q] + nodes->i_per_block - 1) / nodes->i_per_block;
-            cudaGraphKernelNodeSetEnabled(nodes->force[q], nb > 0);
-            if (nb > 0) cudaGraphKernelNodeSetGridDim(nodes->force[q], dim3((unsigned)nb, (unsigned)nodes->chunks[q], 1));
+            // few active particles: the tile-split kernel (same partials), else the list kernel
+            const bool ts = nodes->ts_ok[q] && nact[q] <= nodes->ts_max;
+            const int ipb = ts ? nodes->ts_i_per_block : nodes->i_per_block;
+            const int nb = (nact[q] + ipb - 1) / ipb;
+            const dim3 grid((unsigned)nb, (unsigned)nodes->chunks[q], 1);
+            cudaGraphKernelNodeSetEnabled(nodes->force[q], nb > 0 && !ts);
+            if (nb > 0 && !ts) cudaGraphKernelNodeSetGridDim(nodes->force[q], grid);
+            if (nodes->ts_ok[q]) {
+                cudaGraphKernelNodeSetEnabled(nodes->force_ts[q], nb > 0 && ts);
+                if (nb > 0 && ts) cudaGraphKernelNodeSetGridDim(nodes->force_ts[q], grid);
+            }
         }
         cudaGraphSetConditional(cond, done ? 0u : 1u);
     }

@@ -174,6 +174,7 @@ struct nbody_ctx {
     int64_t graph_kernels = 0, graph_force = 0;
     bool prof = false;
     std::vector<cudaEvent_t> prof_ev;  // pairs
+    std::vector<int64_t> prof_ni, prof_nj;   // i and j particles of each timed launch
     size_t prof_used = 0;
     int64_t n_force = 0, n_kernels = 0;
     std::string err;
@@ -257,7 +258,7 @@ bool use_nccl(const nbody_ctx* c) { return c->comm != nullptr; }
 // force pass over chunks [c_first, c_first + c_count) for the shard's local
 // particles, or (block steps) for the n_i active particles listed in ilist
 int launch_force_range(nbody_ctx* c, Shard& s, int32_t c_first, int32_t c_count, int32_t n_i = -1,
-                       const int32_t* ilist = nullptr, const int32_t* n_dev = nullptr) {
+                       const int32_t* ilist = nullptr, const int32_t* n_dev = nullptr, bool tsplit = false) {
     if (n_i < 0) n_i = s.n_loc;
     if (c_count <= 0 || n_i <= 0) return NBODY_OK;
     nb::ForceArgs f;
@@ -288,9 +289,21 @@ int launch_force_range(nbody_ctx* c, Shard& s, int32_t c_first, int32_t c_count,
         e0 = c->prof_ev[c->prof_used];
         e1 = c->prof_ev[c->prof_used + 1];
         c->prof_used += 2;
+        int64_t nj = 0;   // real j particles in chunks c_first .. c_first + c_count - 1 (mod n_chunks)
+        for (int32_t q = 0; q < c_count; ++q) {
+            const int64_t ch = (c_first + q) % s.plan.n_chunks;
+            nj += std::min<int64_t>(c->n, (ch + 1) * s.plan.chunk) - ch * s.plan.chunk;
+        }
+        c->prof_ni.resize(c->prof_used / 2);
+        c->prof_nj.resize(c->prof_used / 2);
+        c->prof_ni.back() = n_i;
+        c->prof_nj.back() = nj;
         CK(c, cudaEventRecord(e0, c->stream));
     }
-    CK(c, nb::launch_force(f, c->eps2f == 0.f, ncomp(c) == 6, c->stream));
+    if (tsplit)
+        CK(c, nb::launch_force_tsplit(f, c->eps2f == 0.f, c->stream));
+    else
+        CK(c, nb::launch_force(f, c->eps2f == 0.f, ncomp(c) == 6, c->stream));
     if (e1) CK(c, cudaEventRecord(e1, c->stream));
     c->n_force++;
     c->n_kernels++;
@@ -677,9 +690,32 @@ int block_step_body(nbody_ctx* c, cudaGraphConditionalHandle cond, const nb::Blo
     return NBODY_OK;
 }
 
+// the tile-split force kernel for n_i active particles? (needs >= 2 tiles per chunk)
+bool use_tsplit(const Shard& s, int64_t n_i) {
+    return s.plan.chunk >= 2 * nb::kTile && n_i <= nb::force_tsplit_max();
+}
+
+// make the force launch just captured on c->stream device-updatable; its handle
+int capture_force_node(nbody_ctx* c, cudaGraphDeviceNode_t* out) {
+    cudaStreamCaptureStatus st;
+    const cudaGraphNode_t* deps = nullptr;
+    size_t nd = 0;
+    CK(c, cudaStreamGetCaptureInfo(c->stream, &st, nullptr, nullptr, &deps, &nd));
+    if (st != cudaStreamCaptureStatusActive || nd != 1)
+        return fail(c, NBODY_ECUDA, "block graph: force node not found in the capture");
+    cudaLaunchAttributeValue av = {};
+    av.deviceUpdatableKernelNode.deviceUpdatable = 1;
+    CK(c, cudaGraphKernelNodeSetAttribute(deps[0], cudaLaunchAttributeDeviceUpdatableKernelNode, &av));
+    cudaLaunchAttributeValue got = {};
+    CK(c, cudaGraphKernelNodeGetAttribute(deps[0], cudaLaunchAttributeDeviceUpdatableKernelNode, &got));
+    *out = got.deviceUpdatableKernelNode.devNode;
+    return NBODY_OK;
+}
+
 // predict, exchange, force on the active sets, correct.  Host loop: n_act[q] are the
-// active counts read back.  Graph capture (n_act == nullptr): every force launch is made
-// device-updatable and its handle recorded in *nodes for the decide kernel.
+// active counts read back, and each shard launches the list or the tile-split force
+// kernel by its count.  Graph capture (n_act == nullptr): both launches are captured,
+// device-updatable, and the decide kernel enables one of them per block step.
 int block_step_rest(nbody_ctx* c, const int32_t* n_act, nb::BlockGraphNodes* nodes) {
     int rc;
     if (use_nccl(c) && (rc = gather_packets(c, c->stream))) return rc;
@@ -687,22 +723,19 @@ int block_step_rest(nbody_ctx* c, const int32_t* n_act, nb::BlockGraphNodes* nod
         Shard& s = c->sh[q];
         const int32_t n_i = n_act ? n_act[q] : std::max<int32_t>(1, s.n_loc);
         if (n_i <= 0 || s.n_loc <= 0) continue;
-        if ((rc = launch_force_range(c, s, 0, (int32_t)s.plan.n_chunks, n_i, s.ilist, c->nact + q)))
-            return rc;
+        const int32_t nch = (int32_t)s.plan.n_chunks;
         if (nodes) {
-            cudaStreamCaptureStatus st;
-            const cudaGraphNode_t* deps = nullptr;
-            size_t nd = 0;
-            CK(c, cudaStreamGetCaptureInfo(c->stream, &st, nullptr, nullptr, &deps, &nd));
-            if (st != cudaStreamCaptureStatusActive || nd != 1)
-                return fail(c, NBODY_ECUDA, "block graph: force node not found in the capture");
-            cudaLaunchAttributeValue av = {};
-            av.deviceUpdatableKernelNode.deviceUpdatable = 1;
-            CK(c, cudaGraphKernelNodeSetAttribute(deps[0], cudaLaunchAttributeDeviceUpdatableKernelNode, &av));
-            cudaLaunchAttributeValue got = {};
-            CK(c, cudaGraphKernelNodeGetAttribute(deps[0], cudaLaunchAttributeDeviceUpdatableKernelNode, &got));
-            nodes->force[q] = got.deviceUpdatableKernelNode.devNode;
-            nodes->chunks[q] = (int32_t)s.plan.n_chunks;
+            if ((rc = launch_force_range(c, s, 0, nch, n_i, s.ilist, c->nact + q)) ||
+                (rc = capture_force_node(c, &nodes->force[q])))
+                return rc;
+            nodes->chunks[q] = nch;
+            nodes->ts_ok[q] = nb::force_tsplit_max() > 0 && use_tsplit(s, 1) ? 1 : 0;
+            if (nodes->ts_ok[q] &&
+                ((rc = launch_force_range(c, s, 0, nch, n_i, s.ilist, c->nact + q, true)) ||
+                 (rc = capture_force_node(c, &nodes->force_ts[q]))))
+                return rc;
+        } else if ((rc = launch_force_range(c, s, 0, nch, n_i, s.ilist, c->nact + q, use_tsplit(s, n_i)))) {
+            return rc;
         }
     }
     for (int q = 0; q < c->nshards; ++q) {
@@ -758,6 +791,8 @@ int block_run(nbody_ctx* c, int32_t nsteps) {
             const int64_t nk0 = c->n_kernels, nf0 = c->n_force;
             nb::BlockGraphNodes hn = {};
             hn.i_per_block = nb::force_list_i_per_block();
+            hn.ts_i_per_block = nb::force_tsplit_i_per_block();
+            hn.ts_max = nb::force_tsplit_max();
             rc = block_step_body(c, cond, c->gnodes);
             if (!rc) rc = block_step_rest(c, nullptr, &hn);
             cudaGraph_t body = nullptr;
@@ -983,6 +1018,17 @@ int nbody_prof_launch_times(nbody_ctx* c, double* ms, int64_t cap, int64_t* coun
         float t = 0;
         CK(c, cudaEventElapsedTime(&t, c->prof_ev[2 * q], c->prof_ev[2 * q + 1]));
         ms[q] = t;
+    }
+    if (count) *count = nrec;
+    return NBODY_OK;
+}
+
+int nbody_prof_launch_sizes(nbody_ctx* c, int64_t* n_i, int64_t* n_j, int64_t cap, int64_t* count) {
+    if (!c) return fail(nullptr, NBODY_EINVAL, "null context");
+    const int64_t nrec = (int64_t)(c->prof_used / 2);
+    for (int64_t q = 0; q < nrec && q < cap; ++q) {
+        if (n_i) n_i[q] = c->prof_ni[q];
+        if (n_j) n_j[q] = c->prof_nj[q];
     }
     if (count) *count = nrec;
     return NBODY_OK;
