@@ -2,7 +2,7 @@
 """Small end-to-end case for compute-sanitizer (racecheck / memcheck / synccheck):
 every force-kernel instantiation (eps > 0 and eps = 0 guard, Hermite and
 leapfrog, hi/lo, block-step active lists), loopback shards, graph replay and the
-energy kernel, N = 3000.  Also run against the NB_DEBUG_CHECKS=1 library
+energy kernel, N = 3000; block steps at N = 70 001 (tile-split force kernel).  Also run against the NB_DEBUG_CHECKS=1 library
 (tests/test_gpu_debug_checks.py)."""
 import os
 import sys
@@ -24,5 +24,14 @@ for kw in (dict(), dict(integrator="leapfrog"), dict(hilo=True), dict(world=3, l
         s.forces()
         s.step(3)
         s.energy()
+        s.sync()
+# block steps with >= 2 tiles per chunk: the tile-split force kernel (small active sets)
+# and the list kernel; eps > 0 and the eps = 0 guard
+m2, x2, v2 = inputs.parity_round(*inputs.plummer(70001, 4))
+for kw in (dict(integrator="block"), dict(integrator="block", eps=0.0, hilo=False)):
+    eps = kw.pop("eps", 1e-3)
+    with binding.NBody(m2, x2, v2, eps=eps, dt=1 / 256, stream=st, **kw) as s:
+        s.step(1)
+        assert s.block_stats()[0] > 1
         s.sync()
 print("sanitize case ok")
