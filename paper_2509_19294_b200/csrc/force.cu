@@ -548,34 +548,122 @@ __global__ void __launch_bounds__(C::kThreads, kJerk ? C::kMinB : C::kMinBAcc) f
 #undef ACC64
 }
 
-// ---- tile-split active-list kernel (block time steps, small active sets).
+// ---- tile-split kernel: few i, one warp per j-tile.
 // The list kernel gives each CTA a whole chunk (chunk / 256 tiles) of j for
-// its i: with a few active particles the launch has only n_chunks CTAs of
-// one serial j loop each and leaves most of the GPU idle (scripts/
-// block_launch_sizes.py).  Here CTA = (64 active i, chunk) with one warp per
-// tile: every lane holds one packed i-pair (slots ib + lane, ib + 32 + lane),
-// warp w stages tile r0 + w into its own shared-memory buffer and computes
-// that tile's fp32 sums with interact(), and after each round of W tiles the
-// CTA adds the round's tile sums to the fp64 chunk sums in ascending tile
-// order -- the same additions, in the same order, as force_kernel, so the
-// partials are bit-identical to the list kernel's.
+// its i: with a few active particles (block time steps) or a small N the
+// launch has too few CTAs, each one serial j loop, and leaves most of the GPU
+// idle (scripts/block_launch_sizes.py).  Here CTA = (kI i, chunk) with one
+// warp per tile: warp w stages tile r0 + w into its own shared-memory buffer
+// and computes that tile's fp32 sums, and after each round of W tiles the CTA
+// adds the round's tile sums to the fp64 chunk sums in ascending tile order --
+// the same additions, in the same order, as force_kernel, so the partials are
+// bit-identical to every other shape's.
+//   packed (kScalar = false): lane = one i-pair (slots ib + lane, ib + 32 + lane),
+//            interact() as in force_kernel; 64 i per CTA.
+//   scalar (kScalar = true): lane = one i (slot ib + lane), interact1(), the
+//            same operations on one lane; 32 i per CTA.  A warp's j loop is
+//            issue-bound (~26 FP32 instructions per j), and a packed instruction
+//            holds the FMA pipe for two cycles, so the scalar form runs a tile in
+//            about half the time for half the i: it is the faster one when the
+//            launch is latency-bound (tiny active sets, N ~ 1 000).
 constexpr int kTsWarpsMax = 8;
-constexpr int kTsplitMaxDefault = 1024;
-constexpr int kTsI = 64;
-constexpr int kTsNC = 6;
+constexpr int kTsplitMaxDefault = 1024;   // packed tile-split up to this many active i
+constexpr int kTsplit1MaxDefault = 128;   // scalar tile-split up to this many active i
 template <bool kHiLo>
 struct TsCfg {
     static constexpr int kTileB = kTileBytes + (kHiLo ? kLoTileBytes : 0);
-    static constexpr int kOffSum = kTsWarpsMax * kTileB;                       // [W][6][64] fp32
-    static constexpr int kOffAcc = kOffSum + kTsWarpsMax * kTsNC * kTsI * 4;   // [6][64] fp64
-    static constexpr int kSmemBytes = kOffAcc + kTsNC * kTsI * 8;
+    static constexpr int kOffSum = kTsWarpsMax * kTileB;                  // [W][<=6][<=64] fp32
+    static constexpr int kOffAcc = kOffSum + kTsWarpsMax * 6 * 64 * 4;   // [<=6][<=64] fp64
+    static constexpr int kOffBar = kOffAcc + 6 * 64 * 8;                 // one mbarrier per warp
+    static constexpr int kSmemBytes = kOffBar + kTsWarpsMax * 8;
 };
 
-template <bool kGuard, bool kHiLo>
+__device__ __forceinline__ float fadd1(float a, float b) {
+    float d;
+    asm("add.rn.ftz.f32 %0, %1, %2;" : "=f"(d) : "f"(a), "f"(b));
+    return d;
+}
+__device__ __forceinline__ float fmul1(float a, float b) {
+    float d;
+    asm("mul.rn.ftz.f32 %0, %1, %2;" : "=f"(d) : "f"(a), "f"(b));
+    return d;
+}
+__device__ __forceinline__ float ffma1(float a, float b, float c) {
+    float d;
+    asm("fma.rn.ftz.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+    return d;
+}
+
+struct JOps1 {
+    float x, y, z, m, eps2, vx, vy, vz, lx, ly, lz;
+};
+struct IOne {
+    float nx, ny, nz, nvx, nvy, nvz, nlx, nly, nlz;
+};
+template <bool kJerk, bool kHiLo>
+__device__ __forceinline__ JOps1 load_jops1(const JPkt* tile, const float4* tile_lo, int jj) {
+    const float4 P = jpkt_pos(tile[jj]), V = jpkt_vel(tile[jj]);
+    JOps1 j{P.x, P.y, P.z, P.w, V.w, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    if (kJerk) { j.vx = V.x; j.vy = V.y; j.vz = V.z; }
+    if (kHiLo) {
+        const float4 L = tile_lo[jj];
+        j.lx = L.x; j.ly = L.y; j.lz = L.z;
+    }
+    return j;
+}
+
+// interact() on one lane: the same operations in the same order (FTZ, RN), so
+// each lane's tile sum equals the corresponding lane of the packed form
+template <bool kGuard, bool kJerk, bool kHiLo, bool kList, int kNC>
+__device__ __forceinline__ void interact1(const JOps1& j, const IOne& i, float (&acc)[kNC], int sl,
+                                          int64_t jg, const GuardCtx& g) {
+    float dx = fadd1(j.x, i.nx);
+    float dy = fadd1(j.y, i.ny);
+    float dz = fadd1(j.z, i.nz);
+    if (kHiLo) {
+        dx = fadd1(dx, fadd1(j.lx, i.nlx));
+        dy = fadd1(dy, fadd1(j.ly, i.nly));
+        dz = fadd1(dz, fadd1(j.lz, i.nlz));
+    }
+    float s2 = ffma1(dx, dx, j.eps2);
+    s2 = ffma1(dy, dy, s2);
+    s2 = ffma1(dz, dz, s2);
+    float ri = rsqrt_ftz(s2);
+    if (kGuard && s2 == 0.f) {
+        ri = 0.f;
+        report_coincident<kList>(g, sl, jg, j.m);
+    }
+#if FK_RCP
+    float ri2 = rcp_ftz(s2);
+    if (kGuard) ri2 = fmul1(ri, ri);
+#else
+    const float ri2 = fmul1(ri, ri);
+#endif
+    const float mr3 = fmul1(fmul1(j.m, ri), ri2);
+    acc[0] = ffma1(mr3, dx, acc[0]);
+    acc[1] = ffma1(mr3, dy, acc[1]);
+    acc[2] = ffma1(mr3, dz, acc[2]);
+    if (kJerk) {
+        const float wx = fadd1(j.vx, i.nvx);
+        const float wy = fadd1(j.vy, i.nvy);
+        const float wz = fadd1(j.vz, i.nvz);
+        float rv = fmul1(dx, wx);
+        rv = ffma1(dy, wy, rv);
+        rv = ffma1(dz, wz, rv);
+        const float q3 = fmul1(fmul1(rv, ri2), -3.0f);
+        acc[3 % kNC] = ffma1(mr3, ffma1(q3, dx, wx), acc[3 % kNC]);
+        acc[4 % kNC] = ffma1(mr3, ffma1(q3, dy, wy), acc[4 % kNC]);
+        acc[5 % kNC] = ffma1(mr3, ffma1(q3, dz, wz), acc[5 % kNC]);
+    }
+}
+
+template <bool kGuard, bool kJerk, bool kHiLo, bool kScalar, bool kList>
 __global__ void __launch_bounds__(kTsWarpsMax * 32, 2) force_tsplit_kernel(ForceArgs a) {
     using C = TsCfg<kHiLo>;
-    const int n_loc = *a.n_dev;
-    const int ib = (int)blockIdx.x * kTsI;
+    constexpr int kI = kScalar ? 32 : 64, kNC = kJerk ? 6 : 3, kH = kScalar ? 1 : 2;
+    int n_loc = a.n_loc;
+    if constexpr (kList) n_loc = *a.n_dev;   // block steps: active count read on the device
+    const int ib = (int)blockIdx.x * kI;
     if (ib >= n_loc) return;
     extern __shared__ __align__(128) unsigned char smem[];
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, W = (int)blockDim.x >> 5;
@@ -583,79 +671,111 @@ __global__ void __launch_bounds__(kTsWarpsMax * 32, 2) force_tsplit_kernel(Force
     float4* tile_lo = reinterpret_cast<float4*>(smem + w * C::kTileB + kTileBytes);
     float* tsum = reinterpret_cast<float*>(smem + C::kOffSum);
     double* acc64 = reinterpret_cast<double*>(smem + C::kOffAcc);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + C::kOffBar) + w;
+    if (lane == 0) {
+        mbar_init(bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
 
-    float q[2][9];
+    float q[kH][9];
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
+    for (int h = 0; h < kH; ++h) {
         const int il = ib + h * 32 + lane;
         const bool valid = il < n_loc;
-        if (valid) NB_CHECK(a.ilist[il] >= 0 && a.ilist[il] < a.n_loc);
-        load_i<kHiLo>(a, valid, valid ? a.i_base + a.ilist[il] : 0, q[h]);
+        int64_t src = 0;
+        if (valid) {
+            if constexpr (kList) {
+                NB_CHECK(a.ilist[il] >= 0 && a.ilist[il] < a.n_loc);
+                src = a.i_base + a.ilist[il];
+            } else {
+                src = a.i_base + il;
+            }
+        }
+        load_i<kHiLo>(a, valid, src, q[h]);
     }
-    const IPair ip{f2make(q[0][0], q[1][0]), f2make(q[0][1], q[1][1]), f2make(q[0][2], q[1][2]),
-                   f2make(q[0][3], q[1][3]), f2make(q[0][4], q[1][4]), f2make(q[0][5], q[1][5]),
-                   f2make(q[0][6], q[1][6]), f2make(q[0][7], q[1][7]), f2make(q[0][8], q[1][8])};
     const GuardCtx gc{a.ilist, a.i_base, a.coincident, n_loc};
     const f2 m3 = f2bc(-3.0f);
-    for (int k = tid; k < kTsNC * kTsI; k += blockDim.x) acc64[k] = 0.0;
+    IPair ip;
+    IOne i1;
+    if constexpr (kScalar) {
+        i1 = IOne{q[0][0], q[0][1], q[0][2], q[0][3], q[0][4], q[0][5], q[0][6], q[0][7], q[0][8]};
+    } else {
+        ip = IPair{f2make(q[0][0], q[kH - 1][0]), f2make(q[0][1], q[kH - 1][1]), f2make(q[0][2], q[kH - 1][2]),
+                   f2make(q[0][3], q[kH - 1][3]), f2make(q[0][4], q[kH - 1][4]), f2make(q[0][5], q[kH - 1][5]),
+                   f2make(q[0][6], q[kH - 1][6]), f2make(q[0][7], q[kH - 1][7]), f2make(q[0][8], q[kH - 1][8])};
+    }
+    for (int k = tid; k < kNC * kI; k += blockDim.x) acc64[k] = 0.0;
 
     const int c = (a.c_first + (int)blockIdx.y) % a.n_chunks;
     const int64_t jc0 = (int64_t)c * a.chunk;
     const int ntile = a.chunk / kTile;
+    uint32_t phase = 0;
     for (int r0 = 0; r0 < ntile; r0 += W) {
         const int t = r0 + w;
         if (t < ntile) {
-            // stage tile t (L2-resident packets), warp-cooperative 16-B loads
-            const uint4* src = reinterpret_cast<const uint4*>(a.pkt + jc0 + (int64_t)t * kTile);
-            uint4* dst = reinterpret_cast<uint4*>(tile);
-#pragma unroll 4
-            for (int k = lane; k < kTileBytes / 16; k += 32) dst[k] = __ldg(src + k);
-            if (kHiLo) {
-                const uint4* sl = reinterpret_cast<const uint4*>(a.pklo + jc0 + (int64_t)t * kTile);
-                uint4* dl = reinterpret_cast<uint4*>(tile_lo);
-#pragma unroll 4
-                for (int k = lane; k < kLoTileBytes / 16; k += 32) dl[k] = __ldg(sl + k);
+            // stage tile t with one bulk TMA copy (+ the hi/lo tails) on the warp's mbarrier
+            if (lane == 0) {
+                mbar_expect_tx(bar, kTileBytes + (kHiLo ? kLoTileBytes : 0));
+                tma_load_1d(tile, a.pkt + jc0 + (int64_t)t * kTile, kTileBytes, bar);
+                if (kHiLo) tma_load_1d(tile_lo, a.pklo + jc0 + (int64_t)t * kTile, kLoTileBytes, bar);
             }
-            __syncwarp();
-            f2 acc[kTsNC][1];
+            mbar_wait(bar, phase);
+            phase ^= 1;
+            float* ts = tsum + w * kNC * kI;
+            if constexpr (kScalar) {
+                float acc[kNC];
 #pragma unroll
-            for (int k = 0; k < kTsNC; ++k) acc[k][0] = 0ull;
+                for (int k = 0; k < kNC; ++k) acc[k] = 0.f;
 #pragma unroll kUnroll
-            for (int jj = 0; jj < kTile; ++jj) {
-                const JOps jo = load_jops<true, kHiLo>(tile, tile_lo, jj);
-                const int64_t jg = kGuard ? jc0 + (int64_t)t * kTile + jj : 0;
-                interact<kGuard, true, kHiLo, true>(jo, ip, acc, 0, m3, ib + lane, ib + 32 + lane, jg, gc);
-            }
-            float* ts = tsum + w * kTsNC * kTsI;
+                for (int jj = 0; jj < kTile; ++jj) {
+                    const JOps1 jo = load_jops1<kJerk, kHiLo>(tile, tile_lo, jj);
+                    const int64_t jg = kGuard ? jc0 + (int64_t)t * kTile + jj : 0;
+                    interact1<kGuard, kJerk, kHiLo, kList>(jo, i1, acc, ib + lane, jg, gc);
+                }
 #pragma unroll
-            for (int k = 0; k < kTsNC; ++k) {
-                float lo, hi;
-                f2split(acc[k][0], lo, hi);
-                ts[k * kTsI + lane] = lo;
-                ts[k * kTsI + 32 + lane] = hi;
+                for (int k = 0; k < kNC; ++k) ts[k * kI + lane] = acc[k];
+            } else {
+                f2 acc[kNC][1];
+#pragma unroll
+                for (int k = 0; k < kNC; ++k) acc[k][0] = 0ull;
+#pragma unroll kUnroll
+                for (int jj = 0; jj < kTile; ++jj) {
+                    const JOps jo = load_jops<kJerk, kHiLo>(tile, tile_lo, jj);
+                    const int64_t jg = kGuard ? jc0 + (int64_t)t * kTile + jj : 0;
+                    interact<kGuard, kJerk, kHiLo, kList>(jo, ip, acc, 0, m3, ib + lane, ib + 32 + lane, jg, gc);
+                }
+#pragma unroll
+                for (int k = 0; k < kNC; ++k) {
+                    float lo, hi;
+                    f2split(acc[k][0], lo, hi);
+                    ts[k * kI + lane] = lo;
+                    ts[k * kI + 32 + lane] = hi;
+                }
             }
         }
         __syncthreads();   // this round's tile sums are in shared memory
         const int nr = min(W, ntile - r0);
-        for (int k = tid; k < kTsNC * kTsI; k += blockDim.x) {
+        for (int k = tid; k < kNC * kI; k += blockDim.x) {
             double sum = acc64[k];
-            for (int u = 0; u < nr; ++u) sum += (double)tsum[u * kTsNC * kTsI + k];   // ascending tiles
+            for (int u = 0; u < nr; ++u) sum += (double)tsum[u * kNC * kI + k];   // ascending tiles
             acc64[k] = sum;
         }
         __syncthreads();   // tile buffers and tile sums are free for the next round
     }
     NB_CHECK(c >= 0 && c < a.n_chunks);
-    double* out = a.partial + (int64_t)c * kTsNC * a.n_loc_pad;
-    for (int k = tid; k < kTsNC * kTsI; k += blockDim.x) {
-        const int il = ib + k % kTsI;
-        if (il < n_loc) out[(int64_t)(k / kTsI) * a.n_loc_pad + il] = acc64[k];
+    NB_CHECK(ib + kI <= a.n_loc_pad || n_loc <= ib);
+    double* out = a.partial + (int64_t)c * kNC * a.n_loc_pad;
+    for (int k = tid; k < kNC * kI; k += blockDim.x) {
+        const int il = ib + k % kI;
+        if (il < n_loc) out[(int64_t)(k / kI) * a.n_loc_pad + il] = acc64[k];
     }
 }
 
 }  // namespace
 
 int force_i_per_block() { return kIPerBlock; }
-int force_tsplit_i_per_block() { return kTsI; }
+int force_tsplit_i_per_block(bool scalar) { return scalar ? 32 : 64; }
 int force_tsplit_threads(int chunk) { return 32 * std::max(1, std::min(kTsWarpsMax, chunk / kTile)); }
 int force_list_i_per_block() { return CfgSmall::kIPerBlock; }
 int force_hyb() { return kHyb; }
@@ -687,6 +807,28 @@ cudaError_t set_attrs() {
     return e;
 }
 
+template <bool G, bool J, bool H, bool S, bool L>
+cudaError_t set_ts_attr() {
+    return cudaFuncSetAttribute(force_tsplit_kernel<G, J, H, S, L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                TsCfg<H>::kSmemBytes);
+}
+// instantiated: list (block steps, jerk) packed + scalar; plain (small launches) scalar
+template <bool G, bool H>
+cudaError_t set_ts_attrs_gh() {
+    cudaError_t e = set_ts_attr<G, true, H, false, true>();
+    if (e == cudaSuccess) e = set_ts_attr<G, true, H, true, true>();
+    if (e == cudaSuccess) e = set_ts_attr<G, true, H, true, false>();
+    if (e == cudaSuccess) e = set_ts_attr<G, false, H, true, false>();
+    return e;
+}
+cudaError_t set_tsplit_attrs() {
+    cudaError_t e = set_ts_attrs_gh<false, false>();
+    if (e == cudaSuccess) e = set_ts_attrs_gh<false, true>();
+    if (e == cudaSuccess) e = set_ts_attrs_gh<true, false>();
+    if (e == cudaSuccess) e = set_ts_attrs_gh<true, true>();
+    return e;
+}
+
 // dynamic shared memory above 48 KiB must be opted into once per instantiation
 // (a function attribute belongs to the current device's context: once per device)
 cudaError_t ensure_attrs() {
@@ -701,18 +843,7 @@ cudaError_t ensure_attrs() {
     if (done_mask.load(std::memory_order_relaxed) & bit) return cudaSuccess;
     e = set_attrs<CfgBig>();
     if (e == cudaSuccess) e = set_attrs<CfgSmall>();
-    if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(force_tsplit_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 TsCfg<false>::kSmemBytes);
-    if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(force_tsplit_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 TsCfg<true>::kSmemBytes);
-    if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(force_tsplit_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 TsCfg<false>::kSmemBytes);
-    if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(force_tsplit_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 TsCfg<true>::kSmemBytes);
+    if (e == cudaSuccess) e = set_tsplit_attrs();
     if (e == cudaSuccess) done_mask.fetch_or(bit, std::memory_order_release);
     return e;
 }
@@ -769,42 +900,67 @@ bool use_small_cta(const ForceArgs& a) {
     if (kHyb != 0) return false;
     const char* ov = getenv("NBODY_FORCE_CTA");   // tests: small | big (default: by size)
     if (ov && !strcmp(ov, "small")) return true;
-    if (ov && !strcmp(ov, "big")) return false;
+    if (ov && (!strcmp(ov, "big") || !strcmp(ov, "tiny"))) return false;
     const int64_t ctas = (int64_t)((a.n_loc + kIPerBlock - 1) / kIPerBlock) * a.c_count;
     return ctas < 2LL * FK_MINB * sm_count();
+}
+
+// Launches whose 256-i CTAs would not give every SM one CTA (N ~ 1 000) are
+// latency-bound: the scalar tile-split kernel runs them with 32 i per warp.
+bool use_tiny(const ForceArgs& a) {
+    if (kHyb != 0) return false;
+    const char* ov = getenv("NBODY_FORCE_CTA");
+    if (ov && *ov) return !strcmp(ov, "tiny");
+    const int64_t ctas = (int64_t)((a.n_loc + CfgSmall::kIPerBlock - 1) / CfgSmall::kIPerBlock) * a.c_count;
+    return ctas < sm_count();
 }
 
 cudaError_t launch_force(const ForceArgs& a, bool guard_self, bool jerk, cudaStream_t s) {
     if (a.c_count <= 0 || a.n_loc <= 0) return cudaSuccess;
     if (a.ilist) return launch_cfg<CfgSmall>(a, guard_self, jerk, s);   // active-list kernel
 #ifndef FK_NO_SMALL
+    if (use_tiny(a)) return launch_force_tsplit(a, guard_self, jerk, true, s);
     if (use_small_cta(a)) return launch_cfg<CfgSmall>(a, guard_self, jerk, s);
 #endif
     return launch_cfg<CfgBig>(a, guard_self, jerk, s);
 }
 
-template <bool G, bool H>
-cudaError_t launch_tsplit(const ForceArgs& a, cudaStream_t s) {
-    const dim3 grid((unsigned)std::max<int64_t>(1, (a.n_loc + kTsI - 1) / kTsI), (unsigned)a.c_count);
-    force_tsplit_kernel<G, H><<<grid, force_tsplit_threads(a.chunk), TsCfg<H>::kSmemBytes, s>>>(a);
+template <bool G, bool J, bool H, bool S, bool L>
+cudaError_t launch_ts(const ForceArgs& a, cudaStream_t s) {
+    const int ipb = S ? 32 : 64;
+    const dim3 grid((unsigned)std::max<int64_t>(1, (a.n_loc + ipb - 1) / ipb), (unsigned)a.c_count);
+    force_tsplit_kernel<G, J, H, S, L><<<grid, force_tsplit_threads(a.chunk), TsCfg<H>::kSmemBytes, s>>>(a);
     return cudaGetLastError();
 }
+template <bool G, bool H>
+cudaError_t launch_ts_gh(const ForceArgs& a, bool jerk, bool scalar, cudaStream_t s) {
+    if (a.ilist) {   // block steps (jerk)
+        if (!a.n_dev || !jerk) return cudaErrorInvalidValue;
+        return scalar ? launch_ts<G, true, H, true, true>(a, s) : launch_ts<G, true, H, false, true>(a, s);
+    }
+    if (!scalar) return cudaErrorInvalidValue;   // plain launches use the scalar form only
+    return jerk ? launch_ts<G, true, H, true, false>(a, s) : launch_ts<G, false, H, true, false>(a, s);
+}
 
-cudaError_t launch_force_tsplit(const ForceArgs& a, bool guard_self, cudaStream_t s) {
+cudaError_t launch_force_tsplit(const ForceArgs& a, bool guard_self, bool jerk, bool scalar, cudaStream_t s) {
     if (a.c_count <= 0 || a.n_loc <= 0) return cudaSuccess;
-    if (!a.ilist || !a.n_dev) return cudaErrorInvalidValue;   // active-list launches only
     cudaError_t e = ensure_attrs();
     if (e != cudaSuccess) return e;
-    if (guard_self) return a.pklo ? launch_tsplit<true, true>(a, s) : launch_tsplit<true, false>(a, s);
-    return a.pklo ? launch_tsplit<false, true>(a, s) : launch_tsplit<false, false>(a, s);
+    if (guard_self)
+        return a.pklo ? launch_ts_gh<true, true>(a, jerk, scalar, s) : launch_ts_gh<true, false>(a, jerk, scalar, s);
+    return a.pklo ? launch_ts_gh<false, true>(a, jerk, scalar, s) : launch_ts_gh<false, false>(a, jerk, scalar, s);
 }
 
-// Active counts up to this use the tile-split kernel when a chunk has >= 2 tiles
-// (NBODY_TSPLIT_MAX overrides; 0 disables).  Chosen by scripts/block_launch_sizes.py.
-int force_tsplit_max() {
-    const char* e = getenv("NBODY_TSPLIT_MAX");   // read per call: tests switch it per context
-    return e && *e ? std::max(0, atoi(e)) : kTsplitMaxDefault;
+// Block steps: active counts up to force_tsplit1_max() use the scalar tile-split
+// kernel, up to force_tsplit_max() the packed one when a chunk has >= 2 tiles, larger
+// ones the list kernel.  NBODY_TSPLIT1_MAX / NBODY_TSPLIT_MAX override (0 disables;
+// read per call: tests switch them per context).  Chosen by scripts/tsplit_sweep.sh.
+int env_int(const char* name, int dflt) {
+    const char* e = getenv(name);
+    return e && *e ? std::max(0, atoi(e)) : dflt;
 }
+int force_tsplit_max() { return env_int("NBODY_TSPLIT_MAX", kTsplitMaxDefault); }
+int force_tsplit1_max() { return env_int("NBODY_TSPLIT1_MAX", kTsplit1MaxDefault); }
 
 int force_ctas_per_sm(bool jerk, bool hilo) {
     int n = 0;

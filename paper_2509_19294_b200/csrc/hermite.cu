@@ -23,6 +23,8 @@
 // stores per particle.
 #include "internal.h"
 
+#include <algorithm>
+
 #include <math.h>
 
 
@@ -73,7 +75,7 @@ __global__ void pack_state_kernel(StateArgs a) {
 // of kick-drift-kick, vp = v + a dt/2 (the half-step velocity), xp = x + vp dt.
 __device__ __forceinline__ void predict(const StateArgs& a, int i, const double x[3],
                                         const double v[3], const double ac[3],
-                                        const double jk[3]) {
+                                        const double jk[3], double m) {
     const double dt = a.dt, dt2 = dt * dt, dt3 = dt2 * dt;
     double xp[3], vp[3];
     bool ok = true;
@@ -90,7 +92,7 @@ __device__ __forceinline__ void predict(const StateArgs& a, int i, const double 
         ok = ok && isfinite(xp[c]) && isfinite(vp[c]);
     }
     if (!ok) flag_bad(a.bad, a.i_base + i);
-    store_packet(a, a.i_base + i, xp, vp, a.G * a.m[i]);
+    store_packet(a, a.i_base + i, xp, vp, a.G * m);
 }
 
 __global__ void predict_pack_kernel(StateArgs a) {
@@ -102,7 +104,7 @@ __global__ void predict_pack_kernel(StateArgs a) {
             ac[c] = a.a0[c * a.n_loc_pad + i];
             jk[c] = a.j0[c * a.n_loc_pad + i];
         }
-        predict(a, i, x, v, ac, jk);
+        predict(a, i, x, v, ac, jk, a.m[i]);
     }
 }
 
@@ -147,25 +149,36 @@ __global__ void fold_forces_kernel(StateArgs a) {
     }
 }
 
+// kEarly: all state loads before the fold -- best when the pass is latency-bound (small
+// n); with many particles the extra live registers cost the fold's memory parallelism,
+// so large passes load the state after the fold (both before any store)
+template <bool kEarly>
 __global__ void correct_predict_pack_kernel(StateArgs a) {
     const double dt = a.dt, dt2 = dt * dt, dt3 = dt2 * dt, dt4 = dt3 * dt, dt5 = dt4 * dt;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < a.n_loc; i += gridDim.x * blockDim.x) {
-        double x[3], v[3], a1[3], j1[3], f[6];
+        double x[3], v[3], a1[3], j1[3], f[6], a0[3], j0[3], xp[3], vp[3];
         bool ok = true;
-        fold_all(a, i, f);
+        // state loads before any store: at small N this pass is bound by dependent load
+        // round trips, and the stores below would keep the compiler from hoisting them
+        if (!kEarly) fold_all(a, i, f);
+        for (int c = 0; c < 3; ++c) {
+            const int64_t o = c * a.n_loc_pad + i;
+            a0[c] = a.a0[o]; j0[c] = a.j0[o]; xp[c] = a.xp[o]; vp[c] = a.vp[o];
+        }
+        const double mi = a.m[i];
+        if (kEarly) fold_all(a, i, f);
         for (int c = 0; c < 3; ++c) {
             const int64_t o = c * a.n_loc_pad + i;
             a1[c] = f[c];
             j1[c] = f[3 + c];
             if (a.integrator == 0) {   // Hermite corrector (R#3)
-                const double a0 = a.a0[o], j0 = a.j0[o];
-                const double a2 = (-6.0 * (a0 - a1[c]) - dt * (4.0 * j0 + 2.0 * j1[c])) / dt2;
-                const double a3 = (12.0 * (a0 - a1[c]) + 6.0 * dt * (j0 + j1[c])) / dt3;
-                x[c] = a.xp[o] + a2 * dt4 / 24.0 + a3 * dt5 / 120.0;
-                v[c] = a.vp[o] + a2 * dt3 / 6.0 + a3 * dt4 / 24.0;
+                const double a2 = (-6.0 * (a0[c] - a1[c]) - dt * (4.0 * j0[c] + 2.0 * j1[c])) / dt2;
+                const double a3 = (12.0 * (a0[c] - a1[c]) + 6.0 * dt * (j0[c] + j1[c])) / dt3;
+                x[c] = xp[c] + a2 * dt4 / 24.0 + a3 * dt5 / 120.0;
+                v[c] = vp[c] + a2 * dt3 / 6.0 + a3 * dt4 / 24.0;
             } else {                   // leapfrog: closing kick
-                x[c] = a.xp[o];
-                v[c] = a.vp[o] + a1[c] * dt / 2.0;
+                x[c] = xp[c];
+                v[c] = vp[c] + a1[c] * dt / 2.0;
             }
             a.x[o] = x[c];
             a.v[o] = v[c];
@@ -174,7 +187,7 @@ __global__ void correct_predict_pack_kernel(StateArgs a) {
             ok = ok && isfinite(x[c]) && isfinite(v[c]) && isfinite(a1[c]) && isfinite(j1[c]);
         }
         if (!ok) flag_bad(a.bad, a.i_base + i);
-        predict(a, i, x, v, a1, j1);
+        predict(a, i, x, v, a1, j1, mi);
     }
 }
 
@@ -282,16 +295,21 @@ __global__ void block_decide_kernel(long long* ctl, const unsigned long long* tn
     if (nodes) {   // inside the block-step graph
         for (int q = 0; q < nshards; ++q) {
             if (!nodes->force[q]) continue;   // shard without particles: no force node
-            // few active particles: the tile-split kernel (same partials), else the list kernel
-            const bool ts = nodes->ts_ok[q] && nact[q] <= nodes->ts_max;
-            const int ipb = ts ? nodes->ts_i_per_block : nodes->i_per_block;
+            // few active particles: a tile-split kernel (same partials), else the list kernel
+            // (the rule of nbody.cu block_force_kind)
+            const int kind = nact[q] <= nodes->ts1_max ? 2 : (nodes->ts_ok[q] && nact[q] <= nodes->ts_max ? 1 : 0);
+            const int ipb = kind == 2 ? nodes->ts1_i_per_block : kind == 1 ? nodes->ts_i_per_block : nodes->i_per_block;
             const int nb = (nact[q] + ipb - 1) / ipb;
             const dim3 grid((unsigned)nb, (unsigned)nodes->chunks[q], 1);
-            cudaGraphKernelNodeSetEnabled(nodes->force[q], nb > 0 && !ts);
-            if (nb > 0 && !ts) cudaGraphKernelNodeSetGridDim(nodes->force[q], grid);
+            cudaGraphKernelNodeSetEnabled(nodes->force[q], nb > 0 && kind == 0);
+            if (nb > 0 && kind == 0) cudaGraphKernelNodeSetGridDim(nodes->force[q], grid);
             if (nodes->ts_ok[q]) {
-                cudaGraphKernelNodeSetEnabled(nodes->force_ts[q], nb > 0 && ts);
-                if (nb > 0 && ts) cudaGraphKernelNodeSetGridDim(nodes->force_ts[q], grid);
+                cudaGraphKernelNodeSetEnabled(nodes->force_ts[q], nb > 0 && kind == 1);
+                if (nb > 0 && kind == 1) cudaGraphKernelNodeSetGridDim(nodes->force_ts[q], grid);
+            }
+            if (nodes->ts1_max > 0) {
+                cudaGraphKernelNodeSetEnabled(nodes->force_ts1[q], nb > 0 && kind == 2);
+                if (nb > 0 && kind == 2) cudaGraphKernelNodeSetGridDim(nodes->force_ts1[q], grid);
             }
         }
         cudaGraphSetConditional(cond, done ? 0u : 1u);
@@ -312,11 +330,15 @@ __device__ __forceinline__ void select_predict_one(const StateArgs& a, int i, un
     }
     const double D = (double)(int64_t)(tn - (unsigned long long)a.T[i]) * tick;
     const double D2 = D * D, D3 = D2 * D;
-    double xp[3], vp[3];
+    double xp[3], vp[3], xs[3], vs[3], as[3], js[3];
     bool ok = true;
+    for (int c = 0; c < 3; ++c) {   // loads first (see correct_predict_pack_kernel)
+        const int64_t o = c * a.n_loc_pad + i;
+        xs[c] = a.x[o]; vs[c] = a.v[o]; as[c] = a.a0[o]; js[c] = a.j0[o];
+    }
     for (int c = 0; c < 3; ++c) {
         const int64_t o = c * a.n_loc_pad + i;
-        const double x = a.x[o], v = a.v[o], ac = a.a0[o], jk = a.j0[o];
+        const double x = xs[c], v = vs[c], ac = as[c], jk = js[c];
         xp[c] = x + v * D + ac * D2 / 2.0 + jk * D3 / 6.0;
         vp[c] = v + ac * D + jk * D2 / 2.0;
         a.xp[o] = xp[c];
@@ -342,17 +364,21 @@ __device__ __forceinline__ void correct_one(const StateArgs& a, int q, unsigned 
     NB_CHECK(k >= 0 && k <= a.kmax && a.T[i] >= 0);
     const double dt = dt_of(a, k);
     const double dt2 = dt * dt, dt3 = dt2 * dt, dt4 = dt3 * dt, dt5 = dt4 * dt;
-    double s_a1 = 0, s_j1 = 0, s_a2 = 0, s_a3 = 0, f[6];
+    double s_a1 = 0, s_j1 = 0, s_a2 = 0, s_a3 = 0, f[6], a0v[3], j0v[3], xpv[3], vpv[3];
     bool ok = true;
+    for (int c = 0; c < 3; ++c) {   // loads first (see correct_predict_pack_kernel)
+        const int64_t o = c * a.n_loc_pad + i;
+        a0v[c] = a.a0[o]; j0v[c] = a.j0[o]; xpv[c] = a.xp[o]; vpv[c] = a.vp[o];
+    }
     fold_all(a, q, f);
     for (int c = 0; c < 3; ++c) {
         const int64_t o = c * a.n_loc_pad + i;
         const double a1 = f[c], j1 = f[3 + c];
-        const double a0 = a.a0[o], j0 = a.j0[o];
+        const double a0 = a0v[c], j0 = j0v[c];
         const double a2 = (-6.0 * (a0 - a1) - dt * (4.0 * j0 + 2.0 * j1)) / dt2;
         const double a3 = (12.0 * (a0 - a1) + 6.0 * dt * (j0 + j1)) / dt3;
-        const double x = a.xp[o] + a2 * dt4 / 24.0 + a3 * dt5 / 120.0;
-        const double v = a.vp[o] + a2 * dt3 / 6.0 + a3 * dt4 / 24.0;
+        const double x = xpv[c] + a2 * dt4 / 24.0 + a3 * dt5 / 120.0;
+        const double v = vpv[c] + a2 * dt3 / 6.0 + a3 * dt4 / 24.0;
         a.x[o] = x;
         a.v[o] = v;
         a.a0[o] = a1;
@@ -397,62 +423,74 @@ __global__ void block_correct_kernel(StateArgs a, int32_t* reset_nact, int reset
 }
 
 
-unsigned grid_for(int64_t n) {
-    int64_t g = (n + kBlock - 1) / kBlock;
+// launch shape of an O(n) grid-stride pass: 256-thread CTAs, or for small n fewer
+// threads per CTA (a multiple of 32) so that the pass still spreads over ~148 SMs --
+// at N ~ 1 000 these passes are bound by dependent load latency, not bandwidth
+struct Dims {
+    unsigned grid, block;
+};
+Dims dims_for(int64_t n) {
+    if (n < 1) n = 1;
+    int64_t block = kBlock;
+    if (n < 148LL * kBlock) block = std::max<int64_t>(32, (n + 148 * 32 - 1) / (148 * 32) * 32);
+    int64_t g = (n + block - 1) / block;
     if (g > 148 * 16) g = 148 * 16;
-    return (unsigned)(g < 1 ? 1 : g);
+    return Dims{(unsigned)g, (unsigned)block};
 }
 
 }  // namespace
 
 cudaError_t launch_validate(const StateArgs& a, unsigned long long* bad2, cudaStream_t s) {
     if (a.n_loc <= 0) return cudaSuccess;
-    validate_kernel<<<grid_for(a.n_loc), kBlock, 0, s>>>(a, bad2);
+    validate_kernel<<<dims_for(a.n_loc).grid, dims_for(a.n_loc).block, 0, s>>>(a, bad2);
     return cudaGetLastError();
 }
 cudaError_t launch_pack_state(const StateArgs& a, cudaStream_t s) {
     if (a.n_loc <= 0) return cudaSuccess;
-    pack_state_kernel<<<grid_for(a.n_loc), kBlock, 0, s>>>(a);
+    pack_state_kernel<<<dims_for(a.n_loc).grid, dims_for(a.n_loc).block, 0, s>>>(a);
     return cudaGetLastError();
 }
 cudaError_t launch_predict_pack(const StateArgs& a, cudaStream_t s) {
     if (a.n_loc <= 0) return cudaSuccess;
-    predict_pack_kernel<<<grid_for(a.n_loc), kBlock, 0, s>>>(a);
+    predict_pack_kernel<<<dims_for(a.n_loc).grid, dims_for(a.n_loc).block, 0, s>>>(a);
     return cudaGetLastError();
 }
 cudaError_t launch_fold_forces(const StateArgs& a, cudaStream_t s) {
     if (a.n_loc <= 0) return cudaSuccess;
-    fold_forces_kernel<<<grid_for(a.n_loc), kBlock, 0, s>>>(a);
+    fold_forces_kernel<<<dims_for(a.n_loc).grid, dims_for(a.n_loc).block, 0, s>>>(a);
     return cudaGetLastError();
 }
 cudaError_t launch_correct_predict_pack(const StateArgs& a, cudaStream_t s) {
     if (a.n_loc <= 0) return cudaSuccess;
-    correct_predict_pack_kernel<<<grid_for(a.n_loc), kBlock, 0, s>>>(a);
+    if (a.n_loc < 148 * kBlock)
+        correct_predict_pack_kernel<true><<<dims_for(a.n_loc).grid, dims_for(a.n_loc).block, 0, s>>>(a);
+    else
+        correct_predict_pack_kernel<false><<<dims_for(a.n_loc).grid, dims_for(a.n_loc).block, 0, s>>>(a);
     return cudaGetLastError();
 }
 cudaError_t launch_block_init_levels(const StateArgs& a, cudaStream_t s) {
     if (a.n_loc <= 0) return cudaSuccess;
-    block_init_levels_kernel<<<grid_for(a.n_loc), kBlock, 0, s>>>(a);
+    block_init_levels_kernel<<<dims_for(a.n_loc).grid, dims_for(a.n_loc).block, 0, s>>>(a);
     return cudaGetLastError();
 }
 cudaError_t launch_block_reset_time(const StateArgs& a, cudaStream_t s) {
     if (a.n_loc <= 0) return cudaSuccess;
-    block_reset_time_kernel<<<grid_for(a.n_loc), kBlock, 0, s>>>(a);
+    block_reset_time_kernel<<<dims_for(a.n_loc).grid, dims_for(a.n_loc).block, 0, s>>>(a);
     return cudaGetLastError();
 }
 cudaError_t launch_block_tnext(const StateArgs& a, cudaStream_t s) {
     if (a.n_loc <= 0) return cudaSuccess;
-    block_tnext_kernel<<<grid_for(a.n_loc), kBlock, 0, s>>>(a);
+    block_tnext_kernel<<<dims_for(a.n_loc).grid, dims_for(a.n_loc).block, 0, s>>>(a);
     return cudaGetLastError();
 }
 cudaError_t launch_block_select_predict(const StateArgs& a, cudaStream_t s) {
     if (a.n_loc <= 0) return cudaSuccess;
-    block_select_predict_kernel<<<grid_for(a.n_loc), kBlock, 0, s>>>(a);
+    block_select_predict_kernel<<<dims_for(a.n_loc).grid, dims_for(a.n_loc).block, 0, s>>>(a);
     return cudaGetLastError();
 }
 cudaError_t launch_block_correct(const StateArgs& a, int32_t* reset_nact, int reset_n, int32_t* done_ctas,
                                  cudaStream_t s) {
-    block_correct_kernel<<<grid_for(a.n_loc > 0 ? a.n_loc : 1), kBlock, 0, s>>>(a, reset_nact, reset_n,
+    block_correct_kernel<<<dims_for(a.n_loc > 0 ? a.n_loc : 1).grid, dims_for(a.n_loc > 0 ? a.n_loc : 1).block, 0, s>>>(a, reset_nact, reset_n,
                                                                                    done_ctas);
     return cudaGetLastError();
 }
@@ -473,7 +511,7 @@ cudaError_t launch_block_decide(long long* ctl, const unsigned long long* tnext,
 cudaError_t launch_fill_padding(JPkt* pkt, float4* pklo, JPkt64* pk64, int64_t from, int64_t to,
                                 float eps2, cudaStream_t s) {
     if (to <= from) return cudaSuccess;
-    fill_padding_kernel<<<grid_for(to - from), kBlock, 0, s>>>(pkt, pklo, pk64, from, to, eps2);
+    fill_padding_kernel<<<dims_for(to - from).grid, dims_for(to - from).block, 0, s>>>(pkt, pklo, pk64, from, to, eps2);
     return cudaGetLastError();
 }
 

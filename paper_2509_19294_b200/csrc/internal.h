@@ -99,13 +99,15 @@ struct ForceArgs {
 cudaError_t launch_force(const ForceArgs& a, bool guard_self, bool jerk, cudaStream_t s);
 int force_i_per_block();
 int force_list_i_per_block();   // i per CTA of the active-list (block-step) force launches
-// Tile-split active-list force pass (block steps with few active particles): same
-// partials, bit for bit, as launch_force with ilist; CTA = (64 active i, chunk), one
-// warp per j-tile.  Needs ilist and n_dev.
-cudaError_t launch_force_tsplit(const ForceArgs& a, bool guard_self, cudaStream_t s);
-int force_tsplit_i_per_block();
+// Tile-split force pass (few i: block steps with small active sets, N ~ 1 000): same
+// partials, bit for bit, as launch_force; CTA = (64 i packed or 32 i scalar, chunk), one
+// warp per j-tile.  With ilist (needs n_dev, jerk) packed or scalar; plain launches
+// scalar only (launch_force picks it for latency-bound sizes).
+cudaError_t launch_force_tsplit(const ForceArgs& a, bool guard_self, bool jerk, bool scalar, cudaStream_t s);
+int force_tsplit_i_per_block(bool scalar);
 int force_tsplit_threads(int chunk);
-int force_tsplit_max();         // largest active count sent to the tile-split kernel
+int force_tsplit_max();         // block steps: largest active count for the packed tile-split kernel
+int force_tsplit1_max();        // ... and for the scalar one
 int force_hyb();   // fp64 i-particles per thread in the force kernel (0: pure FP32)
 // resident force CTAs per SM for the kernel variant (occupancy calculator)
 int force_ctas_per_sm(bool jerk, bool hilo);
@@ -168,11 +170,12 @@ cudaError_t launch_block_set_tend(long long* ctl, unsigned long long t_end, cuda
 // shard's device-updatable force node (disabled when its active set is empty)
 struct BlockGraphNodes {
     cudaGraphDeviceNode_t force[8];      // per shard (loopback shards <= 8 use the graph)
-    cudaGraphDeviceNode_t force_ts[8];   // tile-split launch of the same shard (if ts_ok)
+    cudaGraphDeviceNode_t force_ts[8];   // packed tile-split launch of the same shard (if ts_ok)
+    cudaGraphDeviceNode_t force_ts1[8];  // scalar tile-split launch (if ts1_max > 0)
     int32_t chunks[8];
-    int32_t ts_ok[8];                    // chunk has >= 2 tiles: tile-split kernel usable
-    int32_t i_per_block, ts_i_per_block;
-    int32_t ts_max;                      // active counts <= ts_max take the tile-split node
+    int32_t ts_ok[8];                    // chunk has >= 2 tiles: packed tile-split usable
+    int32_t i_per_block, ts_i_per_block, ts1_i_per_block;
+    int32_t ts_max, ts1_max;             // active counts <= ts1_max: scalar; <= ts_max: packed
 };
 cudaError_t launch_block_decide(long long* ctl, const unsigned long long* tnext, int32_t* nact,
                                 int nshards, cudaGraphConditionalHandle cond,

@@ -257,8 +257,9 @@ bool use_nccl(const nbody_ctx* c) { return c->comm != nullptr; }
 
 // force pass over chunks [c_first, c_first + c_count) for the shard's local
 // particles, or (block steps) for the n_i active particles listed in ilist
+// tsplit: 0 = list / plain kernel, 1 = packed tile-split, 2 = scalar tile-split (block steps)
 int launch_force_range(nbody_ctx* c, Shard& s, int32_t c_first, int32_t c_count, int32_t n_i = -1,
-                       const int32_t* ilist = nullptr, const int32_t* n_dev = nullptr, bool tsplit = false) {
+                       const int32_t* ilist = nullptr, const int32_t* n_dev = nullptr, int tsplit = 0) {
     if (n_i < 0) n_i = s.n_loc;
     if (c_count <= 0 || n_i <= 0) return NBODY_OK;
     nb::ForceArgs f;
@@ -301,7 +302,7 @@ int launch_force_range(nbody_ctx* c, Shard& s, int32_t c_first, int32_t c_count,
         CK(c, cudaEventRecord(e0, c->stream));
     }
     if (tsplit)
-        CK(c, nb::launch_force_tsplit(f, c->eps2f == 0.f, c->stream));
+        CK(c, nb::launch_force_tsplit(f, c->eps2f == 0.f, ncomp(c) == 6, tsplit == 2, c->stream));
     else
         CK(c, nb::launch_force(f, c->eps2f == 0.f, ncomp(c) == 6, c->stream));
     if (e1) CK(c, cudaEventRecord(e1, c->stream));
@@ -690,9 +691,13 @@ int block_step_body(nbody_ctx* c, cudaGraphConditionalHandle cond, const nb::Blo
     return NBODY_OK;
 }
 
-// the tile-split force kernel for n_i active particles? (needs >= 2 tiles per chunk)
-bool use_tsplit(const Shard& s, int64_t n_i) {
-    return s.plan.chunk >= 2 * nb::kTile && n_i <= nb::force_tsplit_max();
+// force kernel for a block step with n_i active particles: 2 = scalar tile-split,
+// 1 = packed tile-split (needs >= 2 tiles per chunk), 0 = list kernel
+bool packed_tsplit_ok(const Shard& s) { return s.plan.chunk >= 2 * nb::kTile && nb::force_tsplit_max() > 0; }
+int block_force_kind(const Shard& s, int64_t n_i) {
+    if (n_i <= nb::force_tsplit1_max()) return 2;
+    if (packed_tsplit_ok(s) && n_i <= nb::force_tsplit_max()) return 1;
+    return 0;
 }
 
 // make the force launch just captured on c->stream device-updatable; its handle
@@ -729,12 +734,16 @@ int block_step_rest(nbody_ctx* c, const int32_t* n_act, nb::BlockGraphNodes* nod
                 (rc = capture_force_node(c, &nodes->force[q])))
                 return rc;
             nodes->chunks[q] = nch;
-            nodes->ts_ok[q] = nb::force_tsplit_max() > 0 && use_tsplit(s, 1) ? 1 : 0;
+            nodes->ts_ok[q] = packed_tsplit_ok(s) ? 1 : 0;
             if (nodes->ts_ok[q] &&
-                ((rc = launch_force_range(c, s, 0, nch, n_i, s.ilist, c->nact + q, true)) ||
+                ((rc = launch_force_range(c, s, 0, nch, n_i, s.ilist, c->nact + q, 1)) ||
                  (rc = capture_force_node(c, &nodes->force_ts[q]))))
                 return rc;
-        } else if ((rc = launch_force_range(c, s, 0, nch, n_i, s.ilist, c->nact + q, use_tsplit(s, n_i)))) {
+            if (nodes->ts1_max > 0 &&
+                ((rc = launch_force_range(c, s, 0, nch, n_i, s.ilist, c->nact + q, 2)) ||
+                 (rc = capture_force_node(c, &nodes->force_ts1[q]))))
+                return rc;
+        } else if ((rc = launch_force_range(c, s, 0, nch, n_i, s.ilist, c->nact + q, block_force_kind(s, n_i)))) {
             return rc;
         }
     }
@@ -791,8 +800,10 @@ int block_run(nbody_ctx* c, int32_t nsteps) {
             const int64_t nk0 = c->n_kernels, nf0 = c->n_force;
             nb::BlockGraphNodes hn = {};
             hn.i_per_block = nb::force_list_i_per_block();
-            hn.ts_i_per_block = nb::force_tsplit_i_per_block();
+            hn.ts_i_per_block = nb::force_tsplit_i_per_block(false);
+            hn.ts1_i_per_block = nb::force_tsplit_i_per_block(true);
             hn.ts_max = nb::force_tsplit_max();
+            hn.ts1_max = nb::force_tsplit1_max();
             rc = block_step_body(c, cond, c->gnodes);
             if (!rc) rc = block_step_rest(c, nullptr, &hn);
             cudaGraph_t body = nullptr;

@@ -1,12 +1,17 @@
-# block-step time per dt_max vs the tile-split threshold NBODY_TSPLIT_MAX (1 GPU)
+# block-step time per dt_max vs the tile-split thresholds (1 GPU):
+#   NBODY_TSPLIT1_MAX (scalar tile-split) x NBODY_TSPLIT_MAX (packed tile-split)
 mkdir -p gpurun_out
-: > gpurun_out/tsplit_sweep.jsonl
-for cfg in C3 C4; do
-  for tmax in 0 256 1024 4096 16384; do
-    NBODY_TSPLIT_MAX=$tmax timeout 600 python bench.py --integrator block --config $cfg --dt-max 0.0078125 \
-      --steps 3 --warmup 3 --no-cpu-baseline --no-e2e 2>/dev/null | tail -1 | \
-      python -c "import sys,json; d=json.loads(sys.stdin.read()); print(json.dumps({'config':'$cfg','tsplit_max':$tmax,'ms_per_dt_max':d['ms_per_step'],'value':d['value'],'block_steps':d['config']['block_steps_per_step']}))" \
-      >> gpurun_out/tsplit_sweep.jsonl
-  done
+out=${1:-gpurun_out/tsplit_sweep.jsonl}
+: > $out
+run() {   # cfg tmax t1max
+  NBODY_TSPLIT_MAX=$2 NBODY_TSPLIT1_MAX=$3 timeout 600 python bench.py --integrator block --config $1 \
+    --dt-max 0.0078125 --steps 3 --warmup 3 --no-cpu-baseline --no-e2e 2>/dev/null | tail -1 | \
+    python -c "import sys,json; d=json.loads(sys.stdin.read()); print(json.dumps({'config':'$1','tsplit_max':$2,'tsplit1_max':$3,'ms_per_dt_max':d['ms_per_step'],'value':d['value'],'block_steps':d['config']['block_steps_per_step']}))" \
+    >> $out
+}
+for cfg in C2 C3 C4; do
+  run $cfg 0 0
+  run $cfg 1024 0
+  for t1 in 32 64 128 256 512; do run $cfg 1024 $t1; done
 done
-cat gpurun_out/tsplit_sweep.jsonl
+cat $out

@@ -173,20 +173,22 @@ def test_block_argument_errors():
         assert e.value.code == binding.NBODY_EINVAL
 
 
-@pytest.mark.parametrize("n", [1000, 5000])
+@pytest.mark.parametrize("n", [1000, 5000, 70001])
 def test_force_cta_shapes_bit_identical(n, monkeypatch):
     """Force launches over few i (block-step active sets, small N) run the 256-i CTA
-    shape, large ones the 1024-i shape (NBODY_FORCE_CTA=small|big overrides the choice).
-    Each i's j loop is the same in both, so forces are bit-identical, and the small shape
-    meets the parity bar against the oracle."""
+    shape, large ones the 1024-i shape, latency-bound ones (fewer 256-i CTAs than SMs) the
+    scalar tile-split kernel (NBODY_FORCE_CTA=small|big|tiny overrides the choice).  Each
+    i's j loop is the same operation sequence in all three, so forces are bit-identical,
+    and each meets the parity bar against the oracle."""
     m, x, v = inputs.parity_round(*inputs.plummer(n, 77))
     out = {}
-    for shape in ("small", "big"):
+    for shape in ("small", "big", "tiny"):
         monkeypatch.setenv("NBODY_FORCE_CTA", shape)
         with binding.NBody(m, x, v, eps=1e-3, dt=1 / 64, hilo=False) as s:
             out[shape] = [t.cpu().numpy() for t in s.forces()]
-    assert np.array_equal(out["small"][0], out["big"][0])
-    assert np.array_equal(out["small"][1], out["big"][1])
+    for shape in ("big", "tiny"):
+        assert np.array_equal(out["small"][0], out[shape][0])
+        assert np.array_equal(out["small"][1], out[shape][1])
     ao, jo = oracle.forces(m, x, v, eps2_of(1e-3))
     from metrics import max_rel
     assert max_rel(out["small"][0], ao) <= 1e-5 and max_rel(out["small"][1], jo) <= 1e-4
@@ -291,29 +293,38 @@ def test_block_execution_paths_bit_identical(monkeypatch):
 
 
 def _run_env(monkeypatch, env, *args, **kw):
-    for k in ("NBODY_NO_GRAPH", "NBODY_TSPLIT_MAX"):
+    for k in ("NBODY_NO_GRAPH", "NBODY_TSPLIT_MAX", "NBODY_TSPLIT1_MAX"):
         monkeypatch.delenv(k, raising=False)
     for k, val in env.items():
         monkeypatch.setenv(k, val)
     return run_block(*args, **kw)
 
 
-@pytest.mark.parametrize("n,dt_max", [(70001, 1 / 128), (300007, 1 / 1024)])
+LIST_ONLY = {"NBODY_TSPLIT_MAX": "0", "NBODY_TSPLIT1_MAX": "0"}
+ALL_PACKED = {"NBODY_TSPLIT_MAX": str(10**9), "NBODY_TSPLIT1_MAX": "0"}
+ALL_SCALAR = {"NBODY_TSPLIT1_MAX": str(10**9)}
+
+
+@pytest.mark.parametrize("n,dt_max", [(9001, 1 / 128), (70001, 1 / 128), (300007, 1 / 1024)])
 def test_block_tile_split_kernel_bit_identical(n, dt_max, monkeypatch):
-    """Block steps with few active particles run the tile-split force kernel (one warp per
-    j-tile, fp64 chunk sums in ascending tile order); it must reproduce the list kernel's
-    partials bit for bit.  N = 70 001: 3 tiles per chunk, ragged last chunk; N = 300 007:
-    10 tiles per chunk, two rounds of 8 warps.  Runs with every block step on the list
-    kernel (NBODY_TSPLIT_MAX=0), every one on the tile-split kernel, the default split,
+    """Block steps with few active particles run a tile-split force kernel (one warp per
+    j-tile, fp64 chunk sums in ascending tile order; packed i-pairs or one i per lane); it
+    must reproduce the list kernel's partials bit for bit.  N = 9 001: one tile per chunk
+    (scalar form only); N = 70 001: 3 tiles per chunk, ragged last chunk; N = 300 007: 10
+    tiles per chunk, two rounds of 8 warps.  Runs with every block step on the list
+    kernel, every one on the packed or on the scalar tile-split kernel, the default split,
     the host-driven loop and 3 loopback shards all give identical states, levels and
     statistics."""
     m, x, v = inputs.parity_round(*inputs.plummer(n, 41))
     args = (m, x, v, 1e-3, dt_max, 1)
-    ref = _run_env(monkeypatch, {"NBODY_TSPLIT_MAX": "0"}, *args)
-    runs = [_run_env(monkeypatch, {"NBODY_TSPLIT_MAX": str(10**9)}, *args),
+    ref = _run_env(monkeypatch, LIST_ONLY, *args)
+    runs = [_run_env(monkeypatch, ALL_SCALAR, *args),
             _run_env(monkeypatch, {}, *args),
-            _run_env(monkeypatch, {"NBODY_TSPLIT_MAX": str(10**9), "NBODY_NO_GRAPH": "1"}, *args),
+            _run_env(monkeypatch, dict(ALL_SCALAR, NBODY_NO_GRAPH="1"), *args),
             _run_env(monkeypatch, {}, *args, world=3, loopback=True)]
+    if n > 65536:
+        runs += [_run_env(monkeypatch, ALL_PACKED, *args),
+                 _run_env(monkeypatch, dict(ALL_PACKED, NBODY_NO_GRAPH="1"), *args)]
     assert ref[3][0] > 1   # several block steps
     for o in runs:
         assert np.array_equal(o[0], ref[0]) and np.array_equal(o[1], ref[1])
@@ -325,6 +336,7 @@ def test_block_tile_split_eps0_guard(monkeypatch):
     kernel (bit-identical run; both report coincident pairs through the same function)."""
     m, x, v = inputs.parity_round(*inputs.uniform_cube(40000, 8))
     args = (m, x, v, 0.0, 1 / 256, 1)
-    ref = _run_env(monkeypatch, {"NBODY_TSPLIT_MAX": "0"}, *args)
-    ts = _run_env(monkeypatch, {"NBODY_TSPLIT_MAX": str(10**9)}, *args)
-    assert np.array_equal(ts[0], ref[0]) and np.array_equal(ts[1], ref[1]) and ts[3] == ref[3]
+    ref = _run_env(monkeypatch, LIST_ONLY, *args)
+    for env in (ALL_PACKED, ALL_SCALAR):
+        ts = _run_env(monkeypatch, env, *args)
+        assert np.array_equal(ts[0], ref[0]) and np.array_equal(ts[1], ref[1]) and ts[3] == ref[3]
