@@ -356,29 +356,54 @@ __global__ void block_select_predict_kernel(StateArgs a) {
         select_predict_one(a, i, tn, tick, a.nact);
 }
 
-// one active slot of the corrector: fold, Hermite corrector with dt_i, Aarseth level
-__device__ __forceinline__ void correct_one(const StateArgs& a, int q, unsigned long long tn) {
-    const int i = a.ilist[q];
-    NB_CHECK(q < a.n_loc && i >= 0 && i < a.n_loc);
+// state of active particle i the corrector reads (loaded before the fold's partials)
+struct CorrIn {
+    double a0[3], j0[3], xp[3], vp[3];
+};
+__device__ __forceinline__ void load_corr_in(const StateArgs& a, int i, CorrIn& in) {
+    for (int c = 0; c < 3; ++c) {
+        const int64_t o = c * a.n_loc_pad + i;
+        in.a0[c] = a.a0[o]; in.j0[c] = a.j0[o]; in.xp[c] = a.xp[o]; in.vp[c] = a.vp[o];
+    }
+}
+
+// fold of slot q's chunk partials by one warp: lane l loads chunk c0 + l of every
+// component (32 chunks in flight per load round instead of one thread's serial walk),
+// then every lane adds the 32 values in ascending chunk order from shuffles -- the same
+// additions, in the same order, as fold_all
+__device__ __forceinline__ void fold_warp(const StateArgs& a, int q, int lane, double out[6]) {
+    const double* p = a.partial + q;
+    const int64_t row = a.n_loc_pad, stride = (int64_t)a.ncomp * a.n_loc_pad;
+    double s[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    for (int c0 = 0; c0 < a.n_chunks; c0 += 32) {
+        const int c = c0 + lane, cnt = min(32, a.n_chunks - c0);
+        double v[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+        if (c < a.n_chunks)
+            for (int k = 0; k < 6; ++k) v[k] = p[c * stride + k * row];
+        for (int u = 0; u < cnt; ++u)
+#pragma unroll
+            for (int k = 0; k < 6; ++k) s[k] += __shfl_sync(0xffffffffu, v[k], u);
+    }
+    for (int k = 0; k < 6; ++k) out[k] = s[k];
+}
+
+// one active slot of the corrector after the fold: Hermite corrector with dt_i, Aarseth level
+__device__ __forceinline__ void correct_slot(const StateArgs& a, int i, const CorrIn& in, const double f[6],
+                                             unsigned long long tn) {
     const int k = a.lev[i];
     NB_CHECK(k >= 0 && k <= a.kmax && a.T[i] >= 0);
     const double dt = dt_of(a, k);
     const double dt2 = dt * dt, dt3 = dt2 * dt, dt4 = dt3 * dt, dt5 = dt4 * dt;
-    double s_a1 = 0, s_j1 = 0, s_a2 = 0, s_a3 = 0, f[6], a0v[3], j0v[3], xpv[3], vpv[3];
+    double s_a1 = 0, s_j1 = 0, s_a2 = 0, s_a3 = 0;
     bool ok = true;
-    for (int c = 0; c < 3; ++c) {   // loads first (see correct_predict_pack_kernel)
-        const int64_t o = c * a.n_loc_pad + i;
-        a0v[c] = a.a0[o]; j0v[c] = a.j0[o]; xpv[c] = a.xp[o]; vpv[c] = a.vp[o];
-    }
-    fold_all(a, q, f);
     for (int c = 0; c < 3; ++c) {
         const int64_t o = c * a.n_loc_pad + i;
         const double a1 = f[c], j1 = f[3 + c];
-        const double a0 = a0v[c], j0 = j0v[c];
+        const double a0 = in.a0[c], j0 = in.j0[c];
         const double a2 = (-6.0 * (a0 - a1) - dt * (4.0 * j0 + 2.0 * j1)) / dt2;
         const double a3 = (12.0 * (a0 - a1) + 6.0 * dt * (j0 + j1)) / dt3;
-        const double x = xpv[c] + a2 * dt4 / 24.0 + a3 * dt5 / 120.0;
-        const double v = vpv[c] + a2 * dt3 / 6.0 + a3 * dt4 / 24.0;
+        const double x = in.xp[c] + a2 * dt4 / 24.0 + a3 * dt5 / 120.0;
+        const double v = in.vp[c] + a2 * dt3 / 6.0 + a3 * dt4 / 24.0;
         a.x[o] = x;
         a.v[o] = v;
         a.a0[o] = a1;
@@ -401,11 +426,37 @@ __device__ __forceinline__ void correct_one(const StateArgs& a, int q, unsigned 
     a.T[i] = (int64_t)tn;
 }
 
+// Active sets up to this size (and at most one slot per warp of the launch) fold one
+// slot per warp (latency-bound regime), larger ones one slot per thread
+// (bandwidth-bound); the results are identical.
+constexpr int kWarpFoldMax = 4096;
+
 __global__ void block_correct_kernel(StateArgs a, int32_t* reset_nact, int reset_n, int32_t* done_ctas) {
     const int32_t n_act = *a.nact;
     const unsigned long long tn = *a.tnext;
-    for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n_act; q += gridDim.x * blockDim.x)
-        correct_one(a, q, tn);
+    const int nw = (int)((gridDim.x * blockDim.x) >> 5);
+    if (n_act <= min(kWarpFoldMax, nw) && a.ncomp == 6) {   // at most one slot per warp
+        const int lane = threadIdx.x & 31;
+        for (int q = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5); q < n_act; q += nw) {
+            const int i = a.ilist[q];
+            NB_CHECK(q < a.n_loc && i >= 0 && i < a.n_loc);
+            CorrIn in;
+            if (lane == 0) load_corr_in(a, i, in);
+            double f[6];
+            fold_warp(a, q, lane, f);
+            if (lane == 0) correct_slot(a, i, in, f, tn);
+        }
+    } else {
+        for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n_act; q += gridDim.x * blockDim.x) {
+            const int i = a.ilist[q];
+            NB_CHECK(q < a.n_loc && i >= 0 && i < a.n_loc);
+            CorrIn in;
+            load_corr_in(a, i, in);   // loads first (see correct_predict_pack_kernel)
+            double f[6];
+            fold_all(a, q, f);
+            correct_slot(a, i, in, f, tn);
+        }
+    }
     // the last CTA of the last shard's launch resets t_next and the active counts for the
     // next block step (every CTA has read them by the time it counts itself done)
     if (reset_nact) {
