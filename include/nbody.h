@@ -210,7 +210,8 @@ int nbody_sync(nbody_ctx* ctx);
  * that launches it; nbody_prof_read blocks, then returns the summed event
  * time of those launches (ms), their count, and the count of all kernels
  * this context launched since the last reset (reset != 0 clears all three
- * after reading).  Any output may be NULL. */
+ * after reading; kernels a block-step CUDA graph launches on the device are
+ * counted from the device's block-step counter).  Any output may be NULL. */
 int nbody_prof_enable(nbody_ctx* ctx, int32_t on);
 int nbody_prof_read(nbody_ctx* ctx, double* force_ms, int64_t* force_launches,
                     int64_t* kernel_launches, int32_t reset);

@@ -177,6 +177,9 @@ struct nbody_ctx {
     std::vector<int64_t> prof_ni, prof_nj;   // i and j particles of each timed launch
     size_t prof_used = 0;
     int64_t n_force = 0, n_kernels = 0;
+    // block-step graph runs launch their kernels on the device: counted at prof_read time
+    // from the block-step counter ctl[1] (minus the host-driven block steps since the reset)
+    int64_t block_graph_calls = 0, block_host_steps = 0, block_steps_at_reset = 0;
     std::string err;
     int sticky = 0;
 };
@@ -752,7 +755,7 @@ int block_step_rest(nbody_ctx* c, const int32_t* n_act, nb::BlockGraphNodes* nod
         CK(c, nb::launch_block_correct(state_args(c, c->sh[q]), last ? c->nact : nullptr, c->nshards,
                                        c->done_ctas, c->stream));
     }
-    c->n_kernels += 1 + 4 * (int64_t)c->nshards;
+    c->n_kernels += 1 + 4 * (int64_t)c->nshards;   // t_next, select, force, correct; decide
     return NBODY_OK;
 }
 
@@ -822,6 +825,7 @@ int block_run(nbody_ctx* c, int32_t nsteps) {
             CK(c, cudaStreamSynchronize(c->stream));   // hn is a stack object
         }
         CK(c, cudaGraphLaunch(c->block_graph, c->stream));
+        c->block_graph_calls++;
         return NBODY_OK;
     }
     // host-driven loop (NCCL ranks, kernel timing, no capturable stream)
@@ -834,6 +838,7 @@ int block_run(nbody_ctx* c, int32_t nsteps) {
         CK(c, cudaStreamSynchronize(c->stream));
         if (*h_done) break;
         if ((rc = block_step_rest(c, h_nact, nullptr))) return rc;
+        c->block_host_steps++;
     }
     return NBODY_OK;
 }
@@ -1011,8 +1016,23 @@ int nbody_prof_read(nbody_ctx* c, double* force_ms, int64_t* force_launches, int
         ms += t;
     }
     if (force_ms) *force_ms = ms;
+    int64_t graph_kernels = 0;
+    if (is_block(c)) {
+        long long steps = 0;
+        CK(c, cudaMemcpy(&steps, c->ctl + 1, sizeof steps, cudaMemcpyDeviceToHost));
+        const int64_t graph_steps = steps - c->block_steps_at_reset - c->block_host_steps;
+        // per block step t_next, select, force, correct per shard and decide; per call one
+        // last iteration (t_next, select, decide, correct) that finds the run done
+        graph_kernels = (4 * (int64_t)c->nshards + 1) * graph_steps +
+                        (3 * (int64_t)c->nshards + 1) * c->block_graph_calls;
+        if (reset) {
+            c->block_steps_at_reset = steps;
+            c->block_host_steps = 0;
+            c->block_graph_calls = 0;
+        }
+    }
     if (force_launches) *force_launches = c->n_force;
-    if (kernel_launches) *kernel_launches = c->n_kernels;
+    if (kernel_launches) *kernel_launches = c->n_kernels + graph_kernels;
     if (reset) {
         c->prof_used = 0;
         c->n_force = 0;

@@ -340,3 +340,28 @@ def test_block_tile_split_eps0_guard(monkeypatch):
     for env in (ALL_PACKED, ALL_SCALAR):
         ts = _run_env(monkeypatch, env, *args)
         assert np.array_equal(ts[0], ref[0]) and np.array_equal(ts[1], ref[1]) and ts[3] == ref[3]
+
+
+def test_block_kernel_count_covers_graph_launches(monkeypatch):
+    """nbody_prof_read's kernel count (bench.py's gpu_launches) includes the kernels the
+    block-step CUDA graph launches on the device: about 4 per block step and shard, as the
+    host-driven loop counts them launch by launch."""
+    m, x, v = inputs.parity_round(*inputs.plummer(4000, 12))
+    counts = {}
+    for mode in ("graph", "host"):
+        monkeypatch.delenv("NBODY_NO_GRAPH", raising=False)
+        if mode == "host":
+            monkeypatch.setenv("NBODY_NO_GRAPH", "1")
+        with binding.NBody(m, x, v, eps=1e-3, dt=1 / 128, integrator="block") as s:
+            s.step(1)
+            s.prof_read(reset=True)
+            s.step(2)
+            _, _, nk = s.prof_read(reset=True)
+            steps = s.block_stats()[0]
+        counts[mode] = (nk, steps)
+    (ng, sg), (nh, sh) = counts["graph"], counts["host"]
+    assert sg == sh and sg > 20
+    # the counter is cumulative over both calls; the second call has roughly 2/3 of them
+    assert ng >= 4 * (sg // 2) and nh >= 4 * (sh // 2), (ng, nh, sg)
+    # graph and host loop differ only in each call's final (done) iteration
+    assert abs(ng - nh) <= 2 * 3, (ng, nh)
