@@ -568,14 +568,17 @@ __global__ void __launch_bounds__(C::kThreads, kJerk ? C::kMinB : C::kMinBAcc) f
 //            launch is latency-bound (tiny active sets, N ~ 1 000).
 constexpr int kTsWarpsMax = 8;
 constexpr int kTsplitMaxDefault = 1024;   // packed tile-split up to this many active i
-constexpr int kTsplit1MaxDefault = 128;   // scalar tile-split up to this many active i
+constexpr int kTsplit1MaxDefault = 256;   // scalar tile-split up to this many active i
+// shared memory of a W-warp CTA (sized by W, so short chunks get more CTAs per SM):
+// [W tile buffers][W x <=6 x <=64 fp32 tile sums][<=6 x <=64 fp64 chunk sums][W mbarriers]
 template <bool kHiLo>
 struct TsCfg {
     static constexpr int kTileB = kTileBytes + (kHiLo ? kLoTileBytes : 0);
-    static constexpr int kOffSum = kTsWarpsMax * kTileB;                  // [W][<=6][<=64] fp32
-    static constexpr int kOffAcc = kOffSum + kTsWarpsMax * 6 * 64 * 4;   // [<=6][<=64] fp64
-    static constexpr int kOffBar = kOffAcc + 6 * 64 * 8;                 // one mbarrier per warp
-    static constexpr int kSmemBytes = kOffBar + kTsWarpsMax * 8;
+    __host__ __device__ static constexpr int off_sum(int W) { return W * kTileB; }
+    __host__ __device__ static constexpr int off_acc(int W) { return off_sum(W) + W * 6 * 64 * 4; }
+    __host__ __device__ static constexpr int off_bar(int W) { return off_acc(W) + 6 * 64 * 8; }
+    __host__ __device__ static constexpr int smem_bytes(int W) { return off_bar(W) + W * 8; }
+    static constexpr int kSmemMax = smem_bytes(kTsWarpsMax);
 };
 
 __device__ __forceinline__ float fadd1(float a, float b) {
@@ -669,9 +672,9 @@ __global__ void __launch_bounds__(kTsWarpsMax * 32, 2) force_tsplit_kernel(Force
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, W = (int)blockDim.x >> 5;
     JPkt* tile = reinterpret_cast<JPkt*>(smem + w * C::kTileB);
     float4* tile_lo = reinterpret_cast<float4*>(smem + w * C::kTileB + kTileBytes);
-    float* tsum = reinterpret_cast<float*>(smem + C::kOffSum);
-    double* acc64 = reinterpret_cast<double*>(smem + C::kOffAcc);
-    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + C::kOffBar) + w;
+    float* tsum = reinterpret_cast<float*>(smem + C::off_sum(W));
+    double* acc64 = reinterpret_cast<double*>(smem + C::off_acc(W));
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + C::off_bar(W)) + w;
     if (lane == 0) {
         mbar_init(bar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -810,7 +813,7 @@ cudaError_t set_attrs() {
 template <bool G, bool J, bool H, bool S, bool L>
 cudaError_t set_ts_attr() {
     return cudaFuncSetAttribute(force_tsplit_kernel<G, J, H, S, L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                TsCfg<H>::kSmemBytes);
+                                TsCfg<H>::kSmemMax);
 }
 // instantiated: list (block steps, jerk) packed + scalar; plain (small launches) scalar
 template <bool G, bool H>
@@ -929,7 +932,8 @@ template <bool G, bool J, bool H, bool S, bool L>
 cudaError_t launch_ts(const ForceArgs& a, cudaStream_t s) {
     const int ipb = S ? 32 : 64;
     const dim3 grid((unsigned)std::max<int64_t>(1, (a.n_loc + ipb - 1) / ipb), (unsigned)a.c_count);
-    force_tsplit_kernel<G, J, H, S, L><<<grid, force_tsplit_threads(a.chunk), TsCfg<H>::kSmemBytes, s>>>(a);
+    const int threads = force_tsplit_threads(a.chunk);
+    force_tsplit_kernel<G, J, H, S, L><<<grid, threads, TsCfg<H>::smem_bytes(threads / 32), s>>>(a);
     return cudaGetLastError();
 }
 template <bool G, bool H>
