@@ -780,7 +780,7 @@ __global__ void __launch_bounds__(kTsWarpsMax * 32, 2) force_tsplit_kernel(Force
 int force_i_per_block() { return kIPerBlock; }
 int force_tsplit_i_per_block(bool scalar) { return scalar ? 32 : 64; }
 int force_tsplit_threads(int chunk) { return 32 * std::max(1, std::min(kTsWarpsMax, chunk / kTile)); }
-int force_list_i_per_block() { return CfgSmall::kIPerBlock; }
+int force_list_i_per_block(bool big) { return big ? CfgBig::kIPerBlock : CfgSmall::kIPerBlock; }
 int force_hyb() { return kHyb; }
 
 int sm_count();
@@ -789,7 +789,7 @@ template <bool G, bool J, bool H, class C>
 cudaError_t set_attr() {
     cudaError_t e = cudaFuncSetAttribute(force_kernel<G, J, H, C>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
-    if constexpr (J && std::is_same<C, CfgSmall>::value)   // active-list variant (block steps)
+    if constexpr (J)   // active-list variant (block steps)
         if (e == cudaSuccess)
             e = cudaFuncSetAttribute(force_kernel<G, J, H, C, true>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
@@ -859,11 +859,11 @@ cudaError_t launch_one(const ForceArgs& a, unsigned c_count, cudaStream_t s) {
     // kernels' register allocation (and speed) is untouched by it
     const dim3 grid((unsigned)std::max<int64_t>(1, (a.n_loc + C::kIPerBlock - 1) / C::kIPerBlock), c_count);
     if (a.ilist) {
-        if constexpr (J && std::is_same<C, CfgSmall>::value) {
+        if constexpr (J) {
             if (!a.n_dev) return cudaErrorInvalidValue;
             force_kernel<G, J, H, C, true><<<grid, C::kThreads, C::kSmemBytes, s>>>(a);
         } else {
-            return cudaErrorInvalidValue;   // block time steps: jerk kernel, small CTA shape
+            return cudaErrorInvalidValue;   // block time steps: jerk kernel
         }
     } else {
         force_kernel<G, J, H, C><<<grid, C::kThreads, C::kSmemBytes, s>>>(a);
@@ -916,6 +916,12 @@ bool use_tiny(const ForceArgs& a) {
     if (ov && *ov) return !strcmp(ov, "tiny");
     const int64_t ctas = (int64_t)((a.n_loc + CfgSmall::kIPerBlock - 1) / CfgSmall::kIPerBlock) * a.c_count;
     return ctas < sm_count();
+}
+
+cudaError_t launch_force_list(const ForceArgs& a, bool guard_self, bool big, cudaStream_t s) {
+    if (a.c_count <= 0 || a.n_loc <= 0) return cudaSuccess;
+    if (!a.ilist) return cudaErrorInvalidValue;
+    return big ? launch_cfg<CfgBig>(a, guard_self, true, s) : launch_cfg<CfgSmall>(a, guard_self, true, s);
 }
 
 cudaError_t launch_force(const ForceArgs& a, bool guard_self, bool jerk, cudaStream_t s) {

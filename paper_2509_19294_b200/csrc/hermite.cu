@@ -297,12 +297,20 @@ __global__ void block_decide_kernel(long long* ctl, const unsigned long long* tn
             if (!nodes->force[q]) continue;   // shard without particles: no force node
             // few active particles: a tile-split kernel (same partials), else the list kernel
             // (the rule of nbody.cu block_force_kind)
-            const int kind = nact[q] <= nodes->ts1_max ? 2 : (nodes->ts_ok[q] && nact[q] <= nodes->ts_max ? 1 : 0);
-            const int ipb = kind == 2 ? nodes->ts1_i_per_block : kind == 1 ? nodes->ts_i_per_block : nodes->i_per_block;
+            const int kind = nact[q] <= nodes->ts1_max                      ? 2
+                             : (nodes->ts_ok[q] && nact[q] <= nodes->ts_max) ? 1
+                             : nact[q] >= nodes->big_min[q]                  ? 3
+                                                                              : 0;
+            const int ipb = kind == 2   ? nodes->ts1_i_per_block
+                            : kind == 1 ? nodes->ts_i_per_block
+                            : kind == 3 ? nodes->big_i_per_block
+                                        : nodes->i_per_block;
             const int nb = (nact[q] + ipb - 1) / ipb;
             const dim3 grid((unsigned)nb, (unsigned)nodes->chunks[q], 1);
             cudaGraphKernelNodeSetEnabled(nodes->force[q], nb > 0 && kind == 0);
             if (nb > 0 && kind == 0) cudaGraphKernelNodeSetGridDim(nodes->force[q], grid);
+            cudaGraphKernelNodeSetEnabled(nodes->force_big[q], nb > 0 && kind == 3);
+            if (nb > 0 && kind == 3) cudaGraphKernelNodeSetGridDim(nodes->force_big[q], grid);
             if (nodes->ts_ok[q]) {
                 cudaGraphKernelNodeSetEnabled(nodes->force_ts[q], nb > 0 && kind == 1);
                 if (nb > 0 && kind == 1) cudaGraphKernelNodeSetGridDim(nodes->force_ts[q], grid);

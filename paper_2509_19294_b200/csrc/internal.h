@@ -98,7 +98,10 @@ struct ForceArgs {
 // (leapfrog, NEXT f1; partial has 3 components).  Returns the launch error.
 cudaError_t launch_force(const ForceArgs& a, bool guard_self, bool jerk, cudaStream_t s);
 int force_i_per_block();
-int force_list_i_per_block();   // i per CTA of the active-list (block-step) force launches
+int force_list_i_per_block(bool big);   // i per CTA of the active-list (block-step) force launches
+// Active-list force pass in the 256-i (big = false) or the 1024-i CTA shape (large active
+// sets: the big shape is ~2.5 % faster per interaction once it fills >= 2 waves).
+cudaError_t launch_force_list(const ForceArgs& a, bool guard_self, bool big, cudaStream_t s);
 // Tile-split force pass (few i: block steps with small active sets, N ~ 1 000): same
 // partials, bit for bit, as launch_force; CTA = (64 i packed or 32 i scalar, chunk), one
 // warp per j-tile.  With ilist (needs n_dev, jerk) packed or scalar; plain launches
@@ -170,11 +173,13 @@ cudaError_t launch_block_set_tend(long long* ctl, unsigned long long t_end, cuda
 // shard's device-updatable force node (disabled when its active set is empty)
 struct BlockGraphNodes {
     cudaGraphDeviceNode_t force[8];      // per shard (loopback shards <= 8 use the graph)
+    cudaGraphDeviceNode_t force_big[8];  // the same list pass in the 1024-i CTA shape
+    int32_t big_min[8];                  // active counts >= big_min take force_big
     cudaGraphDeviceNode_t force_ts[8];   // packed tile-split launch of the same shard (if ts_ok)
     cudaGraphDeviceNode_t force_ts1[8];  // scalar tile-split launch (if ts1_max > 0)
     int32_t chunks[8];
     int32_t ts_ok[8];                    // chunk has >= 2 tiles: packed tile-split usable
-    int32_t i_per_block, ts_i_per_block, ts1_i_per_block;
+    int32_t i_per_block, big_i_per_block, ts_i_per_block, ts1_i_per_block;
     int32_t ts_max, ts1_max;             // active counts <= ts1_max: scalar; <= ts_max: packed
 };
 cudaError_t launch_block_decide(long long* ctl, const unsigned long long* tnext, int32_t* nact,

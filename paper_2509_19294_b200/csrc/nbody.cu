@@ -260,7 +260,8 @@ bool use_nccl(const nbody_ctx* c) { return c->comm != nullptr; }
 
 // force pass over chunks [c_first, c_first + c_count) for the shard's local
 // particles, or (block steps) for the n_i active particles listed in ilist
-// tsplit: 0 = list / plain kernel, 1 = packed tile-split, 2 = scalar tile-split (block steps)
+// tsplit (block steps): 0 = list kernel (256-i CTAs), 1 = packed tile-split, 2 = scalar
+// tile-split, 3 = list kernel (1024-i CTAs); plain launches: 0
 int launch_force_range(nbody_ctx* c, Shard& s, int32_t c_first, int32_t c_count, int32_t n_i = -1,
                        const int32_t* ilist = nullptr, const int32_t* n_dev = nullptr, int tsplit = 0) {
     if (n_i < 0) n_i = s.n_loc;
@@ -304,8 +305,10 @@ int launch_force_range(nbody_ctx* c, Shard& s, int32_t c_first, int32_t c_count,
         c->prof_nj.back() = nj;
         CK(c, cudaEventRecord(e0, c->stream));
     }
-    if (tsplit)
+    if (tsplit == 1 || tsplit == 2)
         CK(c, nb::launch_force_tsplit(f, c->eps2f == 0.f, ncomp(c) == 6, tsplit == 2, c->stream));
+    else if (ilist)
+        CK(c, nb::launch_force_list(f, c->eps2f == 0.f, tsplit == 3, c->stream));
     else
         CK(c, nb::launch_force(f, c->eps2f == 0.f, ncomp(c) == 6, c->stream));
     if (e1) CK(c, cudaEventRecord(e1, c->stream));
@@ -695,11 +698,25 @@ int block_step_body(nbody_ctx* c, cudaGraphConditionalHandle cond, const nb::Blo
 }
 
 // force kernel for a block step with n_i active particles: 2 = scalar tile-split,
-// 1 = packed tile-split (needs >= 2 tiles per chunk), 0 = list kernel
+// 1 = packed tile-split (needs >= 2 tiles per chunk), 3 = list kernel in 1024-i CTAs
+// (from big_min on), 0 = list kernel in 256-i CTAs
 bool packed_tsplit_ok(const Shard& s) { return s.plan.chunk >= 2 * nb::kTile && nb::force_tsplit_max() > 0; }
-int block_force_kind(const Shard& s, int64_t n_i) {
+// smallest active count whose 1024-i CTAs fill four waves of the GPU (NBODY_LISTBIG_MIN
+// overrides; read per call like the tile-split thresholds).  Swept on C3 and C4 block
+// steps: 2 waves (5 120 active at 128 chunks) and 20 000 active (4.3 waves) within
+// 0.5 %, from 2 000 active on slower (profiles/r01_listbig_sweep.jsonl).
+int32_t list_big_min(const nbody_ctx* c, const Shard& s) {
+    const char* e = getenv("NBODY_LISTBIG_MIN");
+    if (e && *e) return std::max(1, atoi(e));
+    static const int per_sm[2] = {nb::force_ctas_per_sm(true, false), nb::force_ctas_per_sm(true, true)};
+    const int64_t waves4 = 4LL * c->sm_count * per_sm[c->pklo != nullptr];
+    const int64_t ib = (waves4 + s.plan.n_chunks - 1) / s.plan.n_chunks;   // i-blocks needed
+    return (int32_t)std::min<int64_t>(INT32_MAX, ib * nb::force_list_i_per_block(true));
+}
+int block_force_kind(const nbody_ctx* c, const Shard& s, int64_t n_i) {
     if (n_i <= nb::force_tsplit1_max()) return 2;
     if (packed_tsplit_ok(s) && n_i <= nb::force_tsplit_max()) return 1;
+    if (n_i >= list_big_min(c, s)) return 3;
     return 0;
 }
 
@@ -736,6 +753,10 @@ int block_step_rest(nbody_ctx* c, const int32_t* n_act, nb::BlockGraphNodes* nod
             if ((rc = launch_force_range(c, s, 0, nch, n_i, s.ilist, c->nact + q)) ||
                 (rc = capture_force_node(c, &nodes->force[q])))
                 return rc;
+            if ((rc = launch_force_range(c, s, 0, nch, n_i, s.ilist, c->nact + q, 3)) ||
+                (rc = capture_force_node(c, &nodes->force_big[q])))
+                return rc;
+            nodes->big_min[q] = list_big_min(c, s);
             nodes->chunks[q] = nch;
             nodes->ts_ok[q] = packed_tsplit_ok(s) ? 1 : 0;
             if (nodes->ts_ok[q] &&
@@ -746,7 +767,7 @@ int block_step_rest(nbody_ctx* c, const int32_t* n_act, nb::BlockGraphNodes* nod
                 ((rc = launch_force_range(c, s, 0, nch, n_i, s.ilist, c->nact + q, 2)) ||
                  (rc = capture_force_node(c, &nodes->force_ts1[q]))))
                 return rc;
-        } else if ((rc = launch_force_range(c, s, 0, nch, n_i, s.ilist, c->nact + q, block_force_kind(s, n_i)))) {
+        } else if ((rc = launch_force_range(c, s, 0, nch, n_i, s.ilist, c->nact + q, block_force_kind(c, s, n_i)))) {
             return rc;
         }
     }
@@ -802,7 +823,8 @@ int block_run(nbody_ctx* c, int32_t nsteps) {
             }
             const int64_t nk0 = c->n_kernels, nf0 = c->n_force;
             nb::BlockGraphNodes hn = {};
-            hn.i_per_block = nb::force_list_i_per_block();
+            hn.i_per_block = nb::force_list_i_per_block(false);
+            hn.big_i_per_block = nb::force_list_i_per_block(true);
             hn.ts_i_per_block = nb::force_tsplit_i_per_block(false);
             hn.ts1_i_per_block = nb::force_tsplit_i_per_block(true);
             hn.ts_max = nb::force_tsplit_max();

@@ -28,8 +28,13 @@ for kw in (dict(), dict(integrator="leapfrog"), dict(hilo=True), dict(world=3, l
 # block steps with >= 2 tiles per chunk: the tile-split force kernel (small active sets)
 # and the list kernel; eps > 0 and the eps = 0 guard
 m2, x2, v2 = inputs.parity_round(*inputs.plummer(70001, 4))
-for kw in (dict(integrator="block"), dict(integrator="block", eps=0.0, hilo=False)):
+for kw in (dict(integrator="block"), dict(integrator="block", eps=0.0, hilo=False),
+           dict(integrator="block", listbig=True)):
     eps = kw.pop("eps", 1e-3)
+    # every list launch in 1024-i CTAs (NBODY_LISTBIG_MIN is read per launch)
+    os.environ["NBODY_LISTBIG_MIN"] = "1" if kw.pop("listbig", False) else ""
+    os.environ["NBODY_TSPLIT1_MAX"] = "0" if os.environ["NBODY_LISTBIG_MIN"] else ""
+    os.environ["NBODY_TSPLIT_MAX"] = "0" if os.environ["NBODY_LISTBIG_MIN"] else ""
     with binding.NBody(m2, x2, v2, eps=eps, dt=1 / 256, stream=st, **kw) as s:
         s.step(1)
         assert s.block_stats()[0] > 1

@@ -293,14 +293,14 @@ def test_block_execution_paths_bit_identical(monkeypatch):
 
 
 def _run_env(monkeypatch, env, *args, **kw):
-    for k in ("NBODY_NO_GRAPH", "NBODY_TSPLIT_MAX", "NBODY_TSPLIT1_MAX"):
+    for k in ("NBODY_NO_GRAPH", "NBODY_TSPLIT_MAX", "NBODY_TSPLIT1_MAX", "NBODY_LISTBIG_MIN"):
         monkeypatch.delenv(k, raising=False)
     for k, val in env.items():
         monkeypatch.setenv(k, val)
     return run_block(*args, **kw)
 
 
-LIST_ONLY = {"NBODY_TSPLIT_MAX": "0", "NBODY_TSPLIT1_MAX": "0"}
+LIST_ONLY = {"NBODY_TSPLIT_MAX": "0", "NBODY_TSPLIT1_MAX": "0", "NBODY_LISTBIG_MIN": str(10**9)}
 ALL_PACKED = {"NBODY_TSPLIT_MAX": str(10**9), "NBODY_TSPLIT1_MAX": "0"}
 ALL_SCALAR = {"NBODY_TSPLIT1_MAX": str(10**9)}
 
@@ -312,9 +312,9 @@ def test_block_tile_split_kernel_bit_identical(n, dt_max, monkeypatch):
     must reproduce the list kernel's partials bit for bit.  N = 9 001: one tile per chunk
     (scalar form only); N = 70 001: 3 tiles per chunk, ragged last chunk; N = 300 007: 10
     tiles per chunk, two rounds of 8 warps.  Runs with every block step on the list
-    kernel, every one on the packed or on the scalar tile-split kernel, the default split,
-    the host-driven loop and 3 loopback shards all give identical states, levels and
-    statistics."""
+    kernel (256-i CTAs, or 1024-i CTAs), every one on the packed or on the scalar
+    tile-split kernel, the default split, the host-driven loop and 3 loopback shards all
+    give identical states, levels and statistics."""
     m, x, v = inputs.parity_round(*inputs.plummer(n, 41))
     args = (m, x, v, 1e-3, dt_max, 1)
     ref = _run_env(monkeypatch, LIST_ONLY, *args)
@@ -325,6 +325,9 @@ def test_block_tile_split_kernel_bit_identical(n, dt_max, monkeypatch):
     if n > 65536:
         runs += [_run_env(monkeypatch, ALL_PACKED, *args),
                  _run_env(monkeypatch, dict(ALL_PACKED, NBODY_NO_GRAPH="1"), *args)]
+    # list kernel in 1024-i CTAs for every list launch, graph and host loop
+    runs += [_run_env(monkeypatch, dict(LIST_ONLY, NBODY_LISTBIG_MIN="1"), *args),
+             _run_env(monkeypatch, dict(LIST_ONLY, NBODY_LISTBIG_MIN="1", NBODY_NO_GRAPH="1"), *args)]
     assert ref[3][0] > 1   # several block steps
     for o in runs:
         assert np.array_equal(o[0], ref[0]) and np.array_equal(o[1], ref[1])
