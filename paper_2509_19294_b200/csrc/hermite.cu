@@ -232,6 +232,32 @@ __device__ __forceinline__ int64_t ticks_of(const StateArgs& a, int k) {
 
 __device__ __forceinline__ double dt_of(const StateArgs& a, int k) { return ldexp(a.dt, -k); }
 
+// Level histogram: one atomic per distinct level in the warp.
+__device__ __forceinline__ void count_level(int32_t* cnt, int k) {
+    const unsigned act = __activemask();
+    const unsigned peers = __match_any_sync(act, k);
+    if ((int)(threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(cnt + k, __popc(peers));
+}
+
+// t_next after block time t (ticks) = the next multiple of the finest occupied level's
+// step.  Equal to min_i (T_i + dt_i) because every particle at level k was last active
+// at the last multiple of its dt_k (levels start at T = 0, halve at any of their own
+// step times, and double only at multiples of the doubled step, R#28), and the steps
+// are nested powers of two.  ~0 when no particle is counted (an empty rank).
+// Called by a whole warp: each lane loads two counters (kmax <= 50), so the finest
+// occupied level costs one L2 round trip.
+__device__ __forceinline__ unsigned long long next_block_time(const int32_t* cnt, int kmax,
+                                                              unsigned long long t) {
+    const int lane = threadIdx.x & 31;
+    const bool o0 = lane <= kmax && __ldcg(cnt + lane) > 0;
+    const bool o1 = lane + 32 <= kmax && __ldcg(cnt + lane + 32) > 0;
+    const unsigned b0 = __ballot_sync(0xffffffffu, o0), b1 = __ballot_sync(0xffffffffu, o1);
+    const int kf = b1 ? 63 - __clz(b1) : (b0 ? 31 - __clz(b0) : -1);
+    if (kf < 0) return ~0ull;
+    const unsigned long long d = 1ull << (kmax - kf);
+    return (t / d + 1) * d;
+}
+
 __device__ __forceinline__ double norm3(const double* p, int64_t stride, int i) {
     const double x = p[i], y = p[stride + i], z = p[2 * stride + i];
     return sqrt(x * x + y * y + z * z);
@@ -246,31 +272,24 @@ __global__ void block_init_levels_kernel(StateArgs a) {
         while (k < a.kmax && dt_of(a, k) > dts) ++k;
         a.lev[i] = k;
         a.T[i] = 0;
+        count_level(a.lvl_cnt, k);
     }
 }
 
 __global__ void block_reset_time_kernel(StateArgs a) {
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < a.n_loc; i += gridDim.x * blockDim.x)
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < a.n_loc; i += gridDim.x * blockDim.x) {
         a.T[i] = 0;
+        count_level(a.lvl_cnt, a.lev[i]);
+    }
 }
 
 // t_next = min_i (t_i + dt_i): exact integer minimum, so order-independent;
 // one atomic per warp after a shuffle reduction
-__global__ void block_tnext_kernel(StateArgs a) {
-    unsigned long long best = ~0ull;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < a.n_loc; i += gridDim.x * blockDim.x) {
-        const unsigned long long t = (unsigned long long)(a.T[i] + ticks_of(a, a.lev[i]));
-        best = t < best ? t : best;
-    }
-    for (int o = 16; o > 0; o >>= 1) {
-        const unsigned long long u = __shfl_xor_sync(0xffffffffu, best, o);
-        best = u < best ? u : best;
-    }
-    if ((threadIdx.x & 31) == 0 && best != ~0ull) atomicMin(a.tnext, best);
-}
 
-__global__ void block_begin_kernel(unsigned long long* tnext, int32_t* nact, int nshards) {
-    if (threadIdx.x == 0) *tnext = ~0ull;
+__global__ void block_begin_kernel(unsigned long long* tnext, int32_t* nact, int nshards,
+                                   const int32_t* lvl_cnt, int kmax) {
+    const unsigned long long t0 = next_block_time(lvl_cnt, kmax, 0);   // 32 threads
+    if (threadIdx.x == 0) *tnext = t0;
     for (int q = threadIdx.x; q < nshards; q += blockDim.x) nact[q] = 0;
 }
 
@@ -331,6 +350,7 @@ __global__ void block_decide_kernel(long long* ctl, const unsigned long long* tn
 // one particle of the active-set selection + prediction pass (append to *nact / ilist)
 __device__ __forceinline__ void select_predict_one(const StateArgs& a, int i, unsigned long long tn,
                                                    double tick, int32_t* nact) {
+    NB_CHECK((unsigned long long)(a.T[i] + ticks_of(a, a.lev[i])) >= tn);   // none left behind
     if ((unsigned long long)(a.T[i] + ticks_of(a, a.lev[i])) == tn) {
         const int slot = atomicAdd(nact, 1);
         NB_CHECK(slot >= 0 && slot < a.n_loc);
@@ -430,6 +450,10 @@ __device__ __forceinline__ void correct_slot(const StateArgs& a, int i, const Co
     } else if (k > 0 && dtc >= 2.0 * dt && tn % (2ull * (unsigned long long)ticks_of(a, k)) == 0) {
         kn = k - 1;
     }
+    if (kn != k) {
+        atomicSub(a.lvl_cnt + k, 1);
+        atomicAdd(a.lvl_cnt + kn, 1);
+    }
     a.lev[i] = kn;
     a.T[i] = (int64_t)tn;
 }
@@ -468,11 +492,18 @@ __global__ void block_correct_kernel(StateArgs a, int32_t* reset_nact, int reset
     // the last CTA of the last shard's launch resets t_next and the active counts for the
     // next block step (every CTA has read them by the time it counts itself done)
     if (reset_nact) {
+        __shared__ int last;
         __syncthreads();
         if (threadIdx.x == 0) {
             __threadfence();
-            if (atomicAdd(done_ctas, 1) == (int)gridDim.x - 1) {
-                *a.tnext = ~0ull;
+            last = atomicAdd(done_ctas, 1) == (int)gridDim.x - 1;
+        }
+        __syncthreads();
+        if (last && threadIdx.x < 32) {
+            __threadfence();   // every CTA's level updates are visible
+            const unsigned long long nt = next_block_time(a.lvl_cnt, a.kmax, tn);
+            if (threadIdx.x == 0) {
+                *a.tnext = nt;
                 for (int q = 0; q < reset_n; ++q) reset_nact[q] = 0;
                 *done_ctas = 0;
                 __threadfence();
@@ -537,11 +568,6 @@ cudaError_t launch_block_reset_time(const StateArgs& a, cudaStream_t s) {
     block_reset_time_kernel<<<dims_for(a.n_loc).grid, dims_for(a.n_loc).block, 0, s>>>(a);
     return cudaGetLastError();
 }
-cudaError_t launch_block_tnext(const StateArgs& a, cudaStream_t s) {
-    if (a.n_loc <= 0) return cudaSuccess;
-    block_tnext_kernel<<<dims_for(a.n_loc).grid, dims_for(a.n_loc).block, 0, s>>>(a);
-    return cudaGetLastError();
-}
 cudaError_t launch_block_select_predict(const StateArgs& a, cudaStream_t s) {
     if (a.n_loc <= 0) return cudaSuccess;
     block_select_predict_kernel<<<dims_for(a.n_loc).grid, dims_for(a.n_loc).block, 0, s>>>(a);
@@ -553,8 +579,9 @@ cudaError_t launch_block_correct(const StateArgs& a, int32_t* reset_nact, int re
                                                                                    done_ctas);
     return cudaGetLastError();
 }
-cudaError_t launch_block_begin(unsigned long long* tnext, int32_t* nact, int nshards, cudaStream_t s) {
-    block_begin_kernel<<<1, 32, 0, s>>>(tnext, nact, nshards);
+cudaError_t launch_block_begin(unsigned long long* tnext, int32_t* nact, int nshards,
+                               const int32_t* lvl_cnt, int kmax, cudaStream_t s) {
+    block_begin_kernel<<<1, 32, 0, s>>>(tnext, nact, nshards, lvl_cnt, kmax);
     return cudaGetLastError();
 }
 cudaError_t launch_block_set_tend(long long* ctl, unsigned long long t_end, cudaStream_t s) {

@@ -138,6 +138,7 @@ struct StateArgs {
     int32_t* ilist;      // [n_loc] active particles (local indices), slot order
     int32_t* nact;       // active count (device counter)
     unsigned long long* tnext;  // next block time in ticks (device, shared by shards)
+    int32_t* lvl_cnt;    // [64] particles per level, all shards (device); t_next derives from it
     long long* ctl;      // block-run control [t_end ticks, block steps, sum of active, done]
     int32_t kmax;
     double eta, eta_s;
@@ -160,11 +161,13 @@ cudaError_t launch_energy(const double4* eall, int64_t n, int64_t i_base,
 int energy_blocks(int32_t n_loc);
 
 // block time steps (hermite.cu, R#28)
+// Both add every local particle's level to lvl_cnt (zeroed by the caller first).
 cudaError_t launch_block_init_levels(const StateArgs& a, cudaStream_t s);  // lev from eta_s, T = 0
 cudaError_t launch_block_reset_time(const StateArgs& a, cudaStream_t s);   // T = 0 (call start)
-cudaError_t launch_block_tnext(const StateArgs& a, cudaStream_t s);        // atomicMin(tnext, T + dt)
-// reset t_next and the active counts of all nshards shards
-cudaError_t launch_block_begin(unsigned long long* tnext, int32_t* nact, int nshards, cudaStream_t s);
+// first t_next of a call (clock at 0) from the level counts; active counts of all nshards
+// shards reset.  Later t_next values come from the corrector's last CTA (same rule).
+cudaError_t launch_block_begin(unsigned long long* tnext, int32_t* nact, int nshards,
+                               const int32_t* lvl_cnt, int kmax, cudaStream_t s);
 // ctl[0] = t_end (start of a call)
 cudaError_t launch_block_set_tend(long long* ctl, unsigned long long t_end, cudaStream_t s);
 // after t_next and the active sets: done = t_next > t_end (then the active counts are zeroed so

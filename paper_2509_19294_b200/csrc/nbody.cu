@@ -158,6 +158,7 @@ struct nbody_ctx {
     // active counts, pinned read-back of both, run statistics
     unsigned long long* tnext = nullptr;
     int32_t* nact = nullptr;
+    int32_t* lvl_cnt = nullptr;   // [64] particles per level, all shards
     nb::BlockGraphNodes* gnodes = nullptr;   // device copy of the graph's force-node handles
     int32_t* done_ctas = nullptr;            // last-CTA counter of the correct kernel
     long long* ctl = nullptr;            // [t_end, block steps, active sum, done] (device)
@@ -249,6 +250,7 @@ nb::StateArgs state_args(nbody_ctx* c, Shard& s) {
     a.ilist = s.ilist;
     a.nact = c->nact ? c->nact + (&s - c->sh.data()) : nullptr;
     a.tnext = c->tnext;
+    a.lvl_cnt = c->lvl_cnt;
     a.ctl = c->ctl;
     a.kmax = c->cfg.kmax;
     a.eta = c->cfg.eta;
@@ -440,6 +442,7 @@ void free_ctx(nbody_ctx* c) {
     }
     cudaFree(c->tnext);
     cudaFree(c->nact);
+    cudaFree(c->lvl_cnt);
     cudaFree(c->ctl);
     cudaFree(c->gnodes);
     cudaFree(c->done_ctas);
@@ -527,6 +530,7 @@ int init_impl(const nbody_config* cfg, const double* m, const double* x, const d
     if ((rc = dalloc(c, &c->flags, 4))) return rc;
     if (is_block(c)) {
         if ((rc = dalloc(c, &c->tnext, 1)) || (rc = dalloc(c, &c->nact, (size_t)c->nshards)) ||
+            (rc = dalloc(c, &c->lvl_cnt, 64)) ||
             (rc = dalloc(c, &c->ctl, 4)) || (rc = dalloc(c, &c->gnodes, 1)) ||
             (rc = dalloc(c, &c->done_ctas, 1)))
             return rc;
@@ -689,7 +693,8 @@ namespace {
 // the last CTA of each block step's corrector)
 int block_step_body(nbody_ctx* c, cudaGraphConditionalHandle cond, const nb::BlockGraphNodes* nodes) {
     int rc;
-    for (auto& s : c->sh) CK(c, nb::launch_block_tnext(state_args(c, s), c->stream));
+    // t_next of this block step was set by the previous step's corrector (or block_begin)
+    // from the level counts; with NCCL ranks it is the minimum over the ranks
     if (use_nccl(c))
         CKNCCL(c, nccl().AllReduce(c->tnext, c->tnext, 1, ncclUint64, ncclMin, c->comm, c->stream));
     for (auto& s : c->sh) CK(c, nb::launch_block_select_predict(state_args(c, s), c->stream));
@@ -776,7 +781,7 @@ int block_step_rest(nbody_ctx* c, const int32_t* n_act, nb::BlockGraphNodes* nod
         CK(c, nb::launch_block_correct(state_args(c, c->sh[q]), last ? c->nact : nullptr, c->nshards,
                                        c->done_ctas, c->stream));
     }
-    c->n_kernels += 1 + 4 * (int64_t)c->nshards;   // t_next, select, force, correct; decide
+    c->n_kernels += 1 + 3 * (int64_t)c->nshards;   // select, force, correct; decide
     return NBODY_OK;
 }
 
@@ -786,6 +791,7 @@ int block_run(nbody_ctx* c, int32_t nsteps) {
     if ((int64_t)nsteps > (INT64_MAX >> (kmax + 1)))
         return fail(c, NBODY_EINVAL, "nsteps * 2^kmax overflows the block clock");
     if ((rc = ensure_forces(c))) return rc;
+    CK(c, cudaMemsetAsync(c->lvl_cnt, 0, 64 * sizeof(int32_t), c->stream));
     for (auto& s : c->sh) {
         if (c->levels_ok)
             CK(c, nb::launch_block_reset_time(state_args(c, s), c->stream));   // all synchronised
@@ -795,7 +801,7 @@ int block_run(nbody_ctx* c, int32_t nsteps) {
     }
     c->levels_ok = true;
     CK(c, nb::launch_block_set_tend(c->ctl, (unsigned long long)nsteps << kmax, c->stream));
-    CK(c, nb::launch_block_begin(c->tnext, c->nact, c->nshards, c->stream));
+    CK(c, nb::launch_block_begin(c->tnext, c->nact, c->nshards, c->lvl_cnt, kmax, c->stream));
     const bool graph_ok = !use_nccl(c) && !c->prof && c->use_graph && c->nshards <= 8 &&
                           c->stream != cudaStreamLegacy && c->stream != cudaStreamPerThread &&
                           c->stream != nullptr;
@@ -1043,10 +1049,10 @@ int nbody_prof_read(nbody_ctx* c, double* force_ms, int64_t* force_launches, int
         long long steps = 0;
         CK(c, cudaMemcpy(&steps, c->ctl + 1, sizeof steps, cudaMemcpyDeviceToHost));
         const int64_t graph_steps = steps - c->block_steps_at_reset - c->block_host_steps;
-        // per block step t_next, select, force, correct per shard and decide; per call one
-        // last iteration (t_next, select, decide, correct) that finds the run done
-        graph_kernels = (4 * (int64_t)c->nshards + 1) * graph_steps +
-                        (3 * (int64_t)c->nshards + 1) * c->block_graph_calls;
+        // per block step select, force, correct per shard and decide; per call one last
+        // iteration (select, decide, correct) that finds the run done
+        graph_kernels = (3 * (int64_t)c->nshards + 1) * graph_steps +
+                        (2 * (int64_t)c->nshards + 1) * c->block_graph_calls;
         if (reset) {
             c->block_steps_at_reset = steps;
             c->block_host_steps = 0;
