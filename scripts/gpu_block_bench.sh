@@ -1,9 +1,9 @@
 # block time-step bench lines (1 GPU) -> gpurun_out/block_bench.jsonl
 mkdir -p gpurun_out
 : > gpurun_out/block_bench.jsonl
-for spec in "C2 --dt-max 0.0078125" "C3 --dt-max 0.0078125" "C4 --dt-max 0.0078125" "C4 --dt-max 0.0009765625"; do
+for spec in "C2 --dt-max 0.0078125" "C3 --dt-max 0.0078125" "C4 --dt-max 0.0078125" "C4 --dt-max 0.0009765625" "C5 --dt-max 0.0078125 --steps 1"; do
   set -- $spec
-  timeout 900 python bench.py --integrator block --config $spec --steps 3 --warmup 3 --no-cpu-baseline 2>gpurun_out/bb_$1.err | tail -1 >> gpurun_out/block_bench.jsonl
+  timeout 900 python bench.py --integrator block --steps 3 --warmup 3 --no-cpu-baseline --config $spec 2>gpurun_out/bb_$1.err | tail -1 >> gpurun_out/block_bench.jsonl
 done
 python - <<'PY'
 import json
