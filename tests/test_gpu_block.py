@@ -334,6 +334,22 @@ def test_block_tile_split_kernel_bit_identical(n, dt_max, monkeypatch):
         assert np.array_equal(o[2], ref[2]) and o[3] == ref[3]
 
 
+@pytest.mark.parametrize("jchunks", [0, 200])
+def test_block_tile_split_plain_positions_and_chunk_counts(jchunks, monkeypatch):
+    """The tile-split and big-CTA list paths with single-float positions (hilo off) and
+    with more chunks than the default 128 (jchunks = 200: the warp fold's second round of
+    chunk partials): bit-identical to the 256-i list kernel."""
+    m, x, v = inputs.parity_round(*inputs.plummer(70001, 43))
+    args = (m, x, v, 1e-3, 1 / 256, 1)
+    kw = dict(hilo=False, jchunks=jchunks)
+    ref = _run_env(monkeypatch, LIST_ONLY, *args, **kw)
+    assert ref[3][0] > 1
+    for env in (ALL_PACKED, ALL_SCALAR, {}, dict(LIST_ONLY, NBODY_LISTBIG_MIN="1")):
+        o = _run_env(monkeypatch, env, *args, **kw)
+        assert np.array_equal(o[0], ref[0]) and np.array_equal(o[1], ref[1])
+        assert np.array_equal(o[2], ref[2]) and o[3] == ref[3]
+
+
 def test_block_tile_split_eps0_guard(monkeypatch):
     """eps = 0 on the tile-split kernel: self terms excluded exactly as by the guarded list
     kernel (bit-identical run; both report coincident pairs through the same function)."""
