@@ -357,7 +357,7 @@ __global__ void __launch_bounds__(C::kThreads, kJerk ? C::kMinB : C::kMinBAcc) f
             if (il < n_loc) {
                 int64_t src = a.i_base + il;
                 if constexpr (kList) {   // block steps: active slot
-                    NB_CHECK(a.ilist[il] >= 0 && a.ilist[il] < a.n_loc);
+                    NB_CHECK(a.ilist[il] >= 0 && a.ilist[il] < a.n_loc_pad);   // a.n_loc may be the active count
                     src = a.i_base + a.ilist[il];
                 }
                 const JPkt pk = a.pkt[src];
@@ -689,7 +689,7 @@ __global__ void __launch_bounds__(kTsWarpsMax * 32, 2) force_tsplit_kernel(Force
         int64_t src = 0;
         if (valid) {
             if constexpr (kList) {
-                NB_CHECK(a.ilist[il] >= 0 && a.ilist[il] < a.n_loc);
+                NB_CHECK(a.ilist[il] >= 0 && a.ilist[il] < a.n_loc_pad);   // a.n_loc may be the active count
                 src = a.i_base + a.ilist[il];
             } else {
                 src = a.i_base + il;
