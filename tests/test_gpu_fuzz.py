@@ -50,3 +50,54 @@ def test_random_case(k):
     for arr_w, arr_1 in zip(out[world], out[1]):
         assert np.array_equal(arr_w, arr_1), (k, world)
     assert all(np.isfinite(t).all() for t in out[1])
+
+
+BLOCK_CASES = list(range(12))
+
+
+@pytest.mark.parametrize("k", BLOCK_CASES)
+def test_random_block_case(k, monkeypatch):
+    """Block time steps over seeded random sizes (one-tile to ten-tile chunks, ragged),
+    softenings, dt_max, eta, shard counts, position modes, chunk counts and force-kernel
+    thresholds: the default run (CUDA graph, default kernel choice) and a host-driven run
+    with random thresholds (other list / tile-split kernels) are bit-identical; small
+    systems also match the oracle's block schedule and state."""
+    rng = np.random.default_rng(7000 + k)
+    n = int(rng.choice([300, 1025, 4097, 40001, 70001, 150001]))
+    eps = float(rng.choice([1e-3, 1e-2]))
+    dt_max = float(rng.choice([1 / 64, 1 / 256]))
+    eta = float(rng.choice([0.01, 0.02, 0.05]))
+    world = int(rng.integers(1, 4))
+    hilo = bool(rng.integers(0, 2)) if n <= 4097 else True
+    jchunks = int(rng.choice([0, 0, 16, 200]))
+    m, x, v = inputs.parity_round(*inputs.plummer(n, 500 + k))
+    kw = dict(eps=eps, dt=dt_max, integrator="block", eta=eta, hilo=hilo, jchunks=jchunks)
+
+    def run(env, world):
+        for key in ("NBODY_NO_GRAPH", "NBODY_TSPLIT_MAX", "NBODY_TSPLIT1_MAX", "NBODY_LISTBIG_MIN"):
+            monkeypatch.delenv(key, raising=False)
+        for key, val in env.items():
+            monkeypatch.setenv(key, val)
+        with binding.NBody(m, x, v, world=world, loopback=world > 1, **kw) as s:
+            s.step(1)
+            xs, vs = (t.cpu().numpy() for t in s.state())
+            st = s.block_stats(levels=True)
+            s.sync()
+        return xs, vs, st[2], st[:2]
+
+    ref = run({}, 1)
+    env = {"NBODY_NO_GRAPH": "1",
+           "NBODY_TSPLIT1_MAX": str(int(rng.choice([0, 64, 10**9]))),
+           "NBODY_TSPLIT_MAX": str(int(rng.choice([0, 512, 10**9]))),
+           "NBODY_LISTBIG_MIN": str(int(rng.choice([1, 3000, 10**9])))}
+    alt = run(env, world)
+    assert np.array_equal(alt[0], ref[0]) and np.array_equal(alt[1], ref[1]), (k, env)
+    assert np.array_equal(alt[2], ref[2]) and alt[3] == ref[3], (k, env)
+    assert np.isfinite(ref[0]).all() and np.isfinite(ref[1]).all()
+    if n <= 1025 and hilo:   # oracle schedule parity needs two-float positions (R#28)
+        e2 = float(np.float32(eps * eps))
+        xo, vo, _, _, lo, so, co = oracle.hermite_block(m, x, v, e2, dt_max, 1, eta=eta, eta_s=0.01,
+                                                        kmax=20)
+        assert abs(ref[3][0] - so[0]) <= 0.05 * so[0] + 2, (k, ref[3], so)
+        # positions agree to the level of a few adjacent-level choices (see test_gpu_block)
+        assert np.max(np.abs(ref[0] - xo)) <= 1e-6, (k, np.max(np.abs(ref[0] - xo)))
