@@ -170,8 +170,11 @@ int nbody_compute_forces(nbody_ctx* ctx, double* acc, double* jerk);
  * criterion (halve as often as needed, double at most once and only when
  * t_next is a multiple of 2 dt_i).  Levels start from eta_s |a| / |j| at the
  * first step after init or nbody_set_state(keep_forces = 0).  Every
- * particle is synchronised at the end of the call.  Blocks once per block
- * step (the active count sizes the force launch).  Collective. */
+ * particle is synchronised at the end of the call.  With world = 1 or
+ * loopback shards the whole call is one CUDA-graph launch that sizes every
+ * force pass on the device (non-blocking, except the first call, which builds
+ * the graph); with NCCL ranks or kernel timing on it blocks once per block
+ * step.  Collective. */
 int nbody_step(nbody_ctx* ctx, int32_t nsteps);
 
 /* Block time steps only: block steps taken and sum over them of the active
