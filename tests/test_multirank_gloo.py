@@ -8,8 +8,9 @@ What the N > 1 GPU path does per rank, exercised without GPUs:
   * the in-place all-gather of equal `slot`-sized packet slices reassembles the
     global j array in global particle order (emulated with gloo all_gather);
   * per-rank forces on the own i-range (oracle) concatenate to the full evaluation;
-  * block time steps: per-rank minima of t_i + dt_i reduced with MIN give the global
-    t_next, and the ranks' active sets partition the global active set;
+  * block time steps: per-rank minima of t_i + dt_i (and the level-count rule the
+    library uses for them) reduced with MIN give the global t_next, and the ranks'
+    active sets partition the global active set;
   * bench.py's timing reduction is a MAX over ranks.
 """
 import os
@@ -80,6 +81,26 @@ def _worker(rank, world, port, n, q):
         act = [None] * world
         dist.all_gather_object(act, mine)
         assert sorted(sum(act, [])) == [int(i) for i in np.nonzero(due == due.min())[0]]
+        #    later block times: the library derives each rank's t_next from its level counts
+        #    (next multiple of the finest occupied level's step after the block time t,
+        #    every particle last active at the last multiple of its own step); MIN over
+        #    ranks of that equals the global min of t_i + dt_i
+        rng = np.random.default_rng(5)
+        lev2 = rng.integers(0, 8, size=n).astype(np.int64)
+        for t in (0, 3 * (1 << 17), (1 << 20) - (1 << 13), 5 * (1 << 12)):
+            d = 1 << (20 - lev2)
+            due2 = (t // d) * d + d
+            cnt = np.bincount(lev2[i0:i1], minlength=21)
+            occ = np.nonzero(cnt)[0]
+            if occ.size:
+                dmin = 1 << (20 - int(occ.max()))
+                local = (t // dmin + 1) * dmin
+            else:
+                local = 2**62
+            assert occ.size == 0 or local == int(due2[i0:i1].min())
+            tn = torch.tensor([local], dtype=torch.int64)
+            dist.all_reduce(tn, op=dist.ReduceOp.MIN)
+            assert int(tn) == int(due2.min()), (t, int(tn), int(due2.min()))
         # 5) max-over-ranks timing reduction (bench.py)
         t = torch.tensor([10.0 + rank, 1.0 * rank], dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
