@@ -67,12 +67,19 @@ namespace {
 #ifndef FK_UNROLL
 #define FK_UNROLL 2
 #endif
+#ifndef FK_TS_UNROLL
+#define FK_TS_UNROLL 4   // j unroll of the packed tile-split form (sweep: profiles/r01_tsplit_unroll.txt)
+#endif
+#ifndef FK_TS1_UNROLL
+#define FK_TS1_UNROLL 8  // j unroll of the scalar tile-split form (sweep: profiles/r01_tsplit_unroll.txt)
+#endif
 #ifndef FK_ACC_SMEM
 #define FK_ACC_SMEM 1
 #endif
 
 constexpr int kStages = FK_STAGES;        // smem ring depth (tiles)
 constexpr int kUnroll = FK_UNROLL;
+constexpr int kTsUnroll = FK_TS_UNROLL, kTs1Unroll = FK_TS1_UNROLL;
 constexpr int kTileBytes = kTile * (int)sizeof(JPkt);
 constexpr int kLoTileBytes = kTile * (int)sizeof(float4);   // hi/lo position tails (NEXT f2)
 static_assert(kStages * 8 <= 64, "mbarrier area");
@@ -730,7 +737,7 @@ __global__ void __launch_bounds__(kTsWarpsMax * 32, 2) force_tsplit_kernel(Force
                 float acc[kNC];
 #pragma unroll
                 for (int k = 0; k < kNC; ++k) acc[k] = 0.f;
-#pragma unroll kUnroll
+#pragma unroll kTs1Unroll
                 for (int jj = 0; jj < kTile; ++jj) {
                     const JOps1 jo = load_jops1<kJerk, kHiLo>(tile, tile_lo, jj);
                     const int64_t jg = kGuard ? jc0 + (int64_t)t * kTile + jj : 0;
@@ -742,7 +749,7 @@ __global__ void __launch_bounds__(kTsWarpsMax * 32, 2) force_tsplit_kernel(Force
                 f2 acc[kNC][1];
 #pragma unroll
                 for (int k = 0; k < kNC; ++k) acc[k][0] = 0ull;
-#pragma unroll kUnroll
+#pragma unroll kTsUnroll
                 for (int jj = 0; jj < kTile; ++jj) {
                     const JOps jo = load_jops<kJerk, kHiLo>(tile, tile_lo, jj);
                     const int64_t jg = kGuard ? jc0 + (int64_t)t * kTile + jj : 0;
