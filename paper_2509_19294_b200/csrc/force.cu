@@ -67,6 +67,12 @@ namespace {
 #ifndef FK_UNROLL
 #define FK_UNROLL 2
 #endif
+#ifndef FK_SMALL_UNROLL
+#define FK_SMALL_UNROLL 2   // j unroll of the 256-i CTA shape
+#endif
+#ifndef FK_SMALL_LIST_UNROLL
+#define FK_SMALL_LIST_UNROLL 4   // ... in its active-list form (profiles/r01_small_unroll.txt)
+#endif
 #ifndef FK_TS_UNROLL
 #define FK_TS_UNROLL 4   // j unroll of the packed tile-split form (sweep: profiles/r01_tsplit_unroll.txt)
 #endif
@@ -89,9 +95,10 @@ static_assert(kStages * 8 <= 64, "mbarrier area");
 // default (1024 i per CTA) and a small one (256 i per CTA) for launches with
 // few i -- block-step active sets and small N -- where 1024-i CTAs would leave
 // most SMs idle.  Every i's j loop is identical in both, so results are too.
-template <int P, int T, int MINB, int MINB_ACC, int HYB>
+template <int P, int T, int MINB, int MINB_ACC, int HYB, int U = FK_UNROLL, int UL = U>
 struct FkCfg {
     static constexpr int kPairs = P, kThreads = T, kMinB = MINB, kMinBAcc = MINB_ACC, kHyb = HYB;
+    static constexpr int kUnrollJ = U, kUnrollList = UL;   // j-loop unroll: plain / active-list
     static constexpr int kIPerBlock = (2 * P + HYB) * T;
     static constexpr int kT64TileBytes = HYB ? kTile * (int)sizeof(JPkt64) : 0;   // fp64 j tiles
     static constexpr int kAccSmemBytes = FK_ACC_SMEM ? 6 * 2 * P * T * 8 : 0;
@@ -103,7 +110,7 @@ struct FkCfg {
     static constexpr int kSmemBytes = kOffAcc + kAccSmemBytes;
 };
 using CfgBig = FkCfg<FK_PAIRS, FK_THREADS, FK_MINB, FK_MINB_ACC, FK_HYB>;
-using CfgSmall = FkCfg<1, 128, 6, 6, 0>;
+using CfgSmall = FkCfg<1, 128, 6, 6, 0, FK_SMALL_UNROLL, FK_SMALL_LIST_UNROLL>;
 constexpr int kIPerBlock = CfgBig::kIPerBlock;
 constexpr int kHyb = CfgBig::kHyb;
 
@@ -460,7 +467,7 @@ __global__ void __launch_bounds__(C::kThreads, kJerk ? C::kMinB : C::kMinBAcc) f
 #pragma unroll
             for (int p = 0; p < kPairs; ++p) acc[k][p] = 0ull;
 
-#pragma unroll kUnroll
+#pragma unroll(kList ? C::kUnrollList : C::kUnrollJ)
         for (int jj = 0; jj < kTile; ++jj) {
             const JOps jo = load_jops<kJerk, kHiLo>(tile, tile_lo, jj);
             const int64_t jg = kGuard ? jc0 + (int64_t)t * kTile + jj : 0;
