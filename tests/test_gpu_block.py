@@ -384,3 +384,30 @@ def test_block_kernel_count_covers_graph_launches(monkeypatch):
     assert ng >= 4 * (sg // 2) and nh >= 4 * (sh // 2), (ng, nh, sg)
     # graph and host loop differ only in each call's final (done) iteration
     assert abs(ng - nh) <= 2 * 3, (ng, nh)
+
+
+def test_prof_launch_sizes_account_for_every_interaction():
+    """nbody_prof_launch_sizes: shared steps launch n_loc x n per force pass; block steps
+    (host-driven while timing) launch one pass per block step whose i counts are the
+    active counts, so they sum to block_stats' active sum, each against all n j."""
+    m, x, v = inputs.parity_round(*inputs.plummer(5000, 21))
+    with binding.NBody(m, x, v, eps=1e-3, dt=1 / 256) as s:
+        s.forces()
+        s.prof_enable(True)
+        s.prof_read(reset=True)
+        s.step(3)
+        ni, nj = s.prof_launch_sizes()
+        t = s.prof_launch_times()
+        s.sync()
+    assert len(ni) == len(t) == 3 and (ni == 5000).all() and (nj == 5000).all() and (t > 0).all()
+    with binding.NBody(m, x, v, eps=1e-3, dt=1 / 128, integrator="block") as s:
+        s.step(1)
+        s.prof_enable(True)
+        bs0, act0 = s.block_stats()
+        s.prof_read(reset=True)
+        s.step(1)
+        ni, nj = s.prof_launch_sizes()
+        bs1, act1 = s.block_stats()
+        s.sync()
+    assert len(ni) == bs1 - bs0 and ni.sum() == act1 - act0 and (nj == 5000).all()
+    assert (ni >= 1).all() and (ni <= 5000).all()
