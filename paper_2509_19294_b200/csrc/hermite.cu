@@ -298,9 +298,16 @@ __global__ void block_set_tend_kernel(long long* ctl, unsigned long long t_end) 
     ctl[3] = 0;
 }
 
+// the force node of shard q for force kind k (0 list, 1 packed tile-split, 2 scalar
+// tile-split, 3 list in 1024-i CTAs)
+__device__ __forceinline__ cudaGraphDeviceNode_t force_node(const BlockGraphNodes* nodes, int q, int k) {
+    return k == 0 ? nodes->force[q] : k == 1 ? nodes->force_ts[q] : k == 2 ? nodes->force_ts1[q]
+                                                                           : nodes->force_big[q];
+}
+
 __global__ void block_decide_kernel(long long* ctl, const unsigned long long* tnext, int32_t* nact,
                                     int nshards, cudaGraphConditionalHandle cond,
-                                    const BlockGraphNodes* nodes) {
+                                    BlockGraphNodes* nodes) {
     const bool done = *tnext > (unsigned long long)ctl[0];
     if (done) {
         for (int q = 0; q < nshards; ++q) nact[q] = 0;
@@ -325,19 +332,22 @@ __global__ void block_decide_kernel(long long* ctl, const unsigned long long* tn
                             : kind == 3 ? nodes->big_i_per_block
                                         : nodes->i_per_block;
             const int nb = (nact[q] + ipb - 1) / ipb;
-            const dim3 grid((unsigned)nb, (unsigned)nodes->chunks[q], 1);
-            cudaGraphKernelNodeSetEnabled(nodes->force[q], nb > 0 && kind == 0);
-            if (nb > 0 && kind == 0) cudaGraphKernelNodeSetGridDim(nodes->force[q], grid);
-            cudaGraphKernelNodeSetEnabled(nodes->force_big[q], nb > 0 && kind == 3);
-            if (nb > 0 && kind == 3) cudaGraphKernelNodeSetGridDim(nodes->force_big[q], grid);
-            if (nodes->ts_ok[q]) {
-                cudaGraphKernelNodeSetEnabled(nodes->force_ts[q], nb > 0 && kind == 1);
-                if (nb > 0 && kind == 1) cudaGraphKernelNodeSetGridDim(nodes->force_ts[q], grid);
+            const int want = nb > 0 ? kind : -1;
+            const int cur = nodes->cur[q];
+            if (cur == -2) {   // first decision after capture: every captured node is enabled
+                for (int k = 0; k < 4; ++k) {
+                    const cudaGraphDeviceNode_t nd = force_node(nodes, q, k);
+                    if ((k != 1 || nodes->ts_ok[q]) && (k != 2 || nodes->ts1_max > 0))
+                        cudaGraphKernelNodeSetEnabled(nd, k == want);
+                }
+            } else if (cur != want) {   // switch nodes only when the kind changes
+                if (cur >= 0) cudaGraphKernelNodeSetEnabled(force_node(nodes, q, cur), false);
+                if (want >= 0) cudaGraphKernelNodeSetEnabled(force_node(nodes, q, want), true);
             }
-            if (nodes->ts1_max > 0) {
-                cudaGraphKernelNodeSetEnabled(nodes->force_ts1[q], nb > 0 && kind == 2);
-                if (nb > 0 && kind == 2) cudaGraphKernelNodeSetGridDim(nodes->force_ts1[q], grid);
-            }
+            if (want >= 0)
+                cudaGraphKernelNodeSetGridDim(force_node(nodes, q, want),
+                                              dim3((unsigned)nb, (unsigned)nodes->chunks[q], 1));
+            nodes->cur[q] = want;
         }
         cudaGraphSetConditional(cond, done ? 0u : 1u);
     }
@@ -590,7 +600,7 @@ cudaError_t launch_block_set_tend(long long* ctl, unsigned long long t_end, cuda
 }
 cudaError_t launch_block_decide(long long* ctl, const unsigned long long* tnext, int32_t* nact,
                                 int nshards, cudaGraphConditionalHandle cond,
-                                const BlockGraphNodes* nodes, cudaStream_t s) {
+                                BlockGraphNodes* nodes, cudaStream_t s) {
     block_decide_kernel<<<1, 1, 0, s>>>(ctl, tnext, nact, nshards, cond, nodes);
     return cudaGetLastError();
 }

@@ -184,10 +184,11 @@ struct BlockGraphNodes {
     int32_t ts_ok[8];                    // chunk has >= 2 tiles: packed tile-split usable
     int32_t i_per_block, big_i_per_block, ts_i_per_block, ts1_i_per_block;
     int32_t ts_max, ts1_max;             // active counts <= ts1_max: scalar; <= ts_max: packed
+    int32_t cur[8];                      // enabled force node per shard (kind, -1 none, -2 unknown)
 };
 cudaError_t launch_block_decide(long long* ctl, const unsigned long long* tnext, int32_t* nact,
                                 int nshards, cudaGraphConditionalHandle cond,
-                                const BlockGraphNodes* nodes, cudaStream_t s);
+                                BlockGraphNodes* nodes, cudaStream_t s);
 
 // active set + every particle predicted to t_next and packed (one pass)
 cudaError_t launch_block_select_predict(const StateArgs& a, cudaStream_t s);

@@ -691,7 +691,7 @@ namespace {
 // with NCCL (or kernel timing on) the host drives the loop and reads `done`.
 // t_next and the active counts start reset (block_begin before the first block step, then
 // the last CTA of each block step's corrector)
-int block_step_body(nbody_ctx* c, cudaGraphConditionalHandle cond, const nb::BlockGraphNodes* nodes) {
+int block_step_body(nbody_ctx* c, cudaGraphConditionalHandle cond, nb::BlockGraphNodes* nodes) {
     int rc;
     // t_next of this block step was set by the previous step's corrector (or block_begin)
     // from the level counts; with NCCL ranks it is the minimum over the ranks
@@ -835,6 +835,7 @@ int block_run(nbody_ctx* c, int32_t nsteps) {
             hn.ts1_i_per_block = nb::force_tsplit_i_per_block(true);
             hn.ts_max = nb::force_tsplit_max();
             hn.ts1_max = nb::force_tsplit1_max();
+            for (int q = 0; q < 8; ++q) hn.cur[q] = -2;
             rc = block_step_body(c, cond, c->gnodes);
             if (!rc) rc = block_step_rest(c, nullptr, &hn);
             cudaGraph_t body = nullptr;
