@@ -337,8 +337,7 @@ __global__ void block_decide_kernel(long long* ctl, const unsigned long long* tn
             if (cur == -2) {   // first decision after capture: every captured node is enabled
                 for (int k = 0; k < 4; ++k) {
                     const cudaGraphDeviceNode_t nd = force_node(nodes, q, k);
-                    if ((k != 1 || nodes->ts_ok[q]) && (k != 2 || nodes->ts1_max > 0))
-                        cudaGraphKernelNodeSetEnabled(nd, k == want);
+                    if (nd) cudaGraphKernelNodeSetEnabled(nd, k == want);   // null: not captured
                 }
             } else if (cur != want) {   // switch nodes only when the kind changes
                 if (cur >= 0) cudaGraphKernelNodeSetEnabled(force_node(nodes, q, cur), false);

@@ -758,10 +758,16 @@ int block_step_rest(nbody_ctx* c, const int32_t* n_act, nb::BlockGraphNodes* nod
             if ((rc = launch_force_range(c, s, 0, nch, n_i, s.ilist, c->nact + q)) ||
                 (rc = capture_force_node(c, &nodes->force[q])))
                 return rc;
-            if ((rc = launch_force_range(c, s, 0, nch, n_i, s.ilist, c->nact + q, 3)) ||
-                (rc = capture_force_node(c, &nodes->force_big[q])))
-                return rc;
+            // the 1024-i list node only where an active set can reach big_min (a disabled
+            // node still costs the graph a little every block step)
             nodes->big_min[q] = list_big_min(c, s);
+            if (nodes->big_min[q] <= s.n_loc) {
+                if ((rc = launch_force_range(c, s, 0, nch, n_i, s.ilist, c->nact + q, 3)) ||
+                    (rc = capture_force_node(c, &nodes->force_big[q])))
+                    return rc;
+            } else {
+                nodes->big_min[q] = INT32_MAX;
+            }
             nodes->chunks[q] = nch;
             nodes->ts_ok[q] = packed_tsplit_ok(s) ? 1 : 0;
             if (nodes->ts_ok[q] &&
