@@ -337,6 +337,23 @@ def test_cuda_graph_replay_bit_identical(monkeypatch):
     assert np.array_equal(out[0][0], out[1][0]) and np.array_equal(out[0][1], out[1][1])
 
 
+@pytest.mark.parametrize("integrator", ["hermite", "leapfrog", "block"])
+def test_runtime_non_finite_state_is_reported_and_sticky(integrator):
+    """Fault injection through the step size: dt = 1e200 is a valid argument, but the
+    predictor's dt^3 term overflows, so the fp64 update kernels flag a non-finite state;
+    the next blocking call returns NBODY_ENONFINITE naming a particle, and every later
+    call on the context NBODY_ESTATE."""
+    m, x, v = inputs.make("C1")
+    with binding.NBody(m, x, v, eps=1e-2, dt=1e200, integrator=integrator) as s:
+        with pytest.raises(binding.NBodyError) as e:
+            s.step(1)
+            s.sync()
+        assert e.value.code == binding.NBODY_ENONFINITE and "non-finite state at particle" in str(e.value)
+        with pytest.raises(binding.NBodyError) as e2:
+            s.forces()
+        assert e2.value.code == binding.NBODY_ESTATE
+
+
 def test_c_abi_argument_errors():
     """EINVAL paths of the C-ABI with a live context (messages name the problem)."""
     m, x, v = inputs.make("C1")
