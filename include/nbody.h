@@ -177,6 +177,26 @@ int nbody_compute_forces(nbody_ctx* ctx, double* acc, double* jerk);
  * step.  Collective. */
 int nbody_step(nbody_ctx* ctx, int32_t nsteps);
 
+/* Checkpoint / exact resume.  The state between steps is (x, v) plus the
+ * derivatives the next step starts from: a0, j0 of the last P(EC)^1 step,
+ * evaluated at the predicted positions, so re-evaluating them at the
+ * corrected state (what a fresh nbody_init does) changes the next step in
+ * the last bits.  nbody_get_derivs copies them ([3][i1 - i0] each, host or
+ * device; evaluated first if no step or force call has produced them; jerk
+ * ignored for the leapfrog integrator, may be NULL), blocking for host
+ * pointers.  nbody_set_derivs restores them into a context holding the
+ * same (x, v) (after nbody_init or nbody_set_state): the next nbody_step
+ * then continues bit for bit as the saved run would have (checks
+ * finiteness: NBODY_EINVAL naming the index; jerk required for the Hermite
+ * integrators).  nbody_set_levels (block time steps only) restores every
+ * local particle's level k_i (int32 [i1 - i0], host or device; NBODY_EINVAL
+ * naming a level outside [0, kmax]) so the next nbody_step keeps them instead
+ * of restarting from eta_s.  A saved block run is (x, v, a0, j0, levels) at
+ * a call boundary, where every particle is synchronised.  Blocks. */
+int nbody_get_derivs(nbody_ctx* ctx, double* acc, double* jerk);
+int nbody_set_derivs(nbody_ctx* ctx, const double* acc, const double* jerk);
+int nbody_set_levels(nbody_ctx* ctx, const int32_t* level);
+
 /* Block time steps only: block steps taken and sum over them of the active
  * count since init (either may be NULL), and the current level k_i of every
  * local particle (level: int32 [i1 - i0], host or device, may be NULL; all

@@ -23,6 +23,7 @@ EXPORTS = (
     "nbody_compute_forces", "nbody_step", "nbody_energy", "nbody_get_state",
     "nbody_set_state", "nbody_sync", "nbody_prof_enable", "nbody_prof_read",
     "nbody_prof_launch_times", "nbody_prof_launch_sizes", "nbody_block_stats",
+    "nbody_get_derivs", "nbody_set_derivs", "nbody_set_levels",
     "nbody_last_error", "nbody_destroy",
 )
 
@@ -98,6 +99,9 @@ def lib():
         "nbody_prof_launch_times": ([p, p, i64, P64], ctypes.c_int),
         "nbody_prof_launch_sizes": ([p, p, p, i64, P64], ctypes.c_int),
         "nbody_block_stats": ([p, P64, P64, p], ctypes.c_int),
+        "nbody_get_derivs": ([p, p, p], ctypes.c_int),
+        "nbody_set_derivs": ([p, p, p], ctypes.c_int),
+        "nbody_set_levels": ([p, p], ctypes.c_int),
         "nbody_last_error": ([p], ctypes.c_char_p),
         "nbody_destroy": ([p], None),
     }
@@ -250,6 +254,31 @@ class NBody:
         _want(x, (3, self.n_loc), "x")
         _want(v, (3, self.n_loc), "v")
         self._c(lib().nbody_set_state(self._ctx, _ptr(x), _ptr(v), 1 if keep_forces else 0))
+
+    def derivs(self, acc=None, jerk=None):
+        """(acc, jerk) the next step starts from, (3, n_loc) float64 (checkpointing)."""
+        import torch
+        if acc is None:
+            acc = torch.empty((3, self.n_loc), dtype=torch.float64, device=self.device)
+        if jerk is None:
+            jerk = torch.empty((3, self.n_loc), dtype=torch.float64, device=self.device)
+        _want(acc, (3, self.n_loc), "acc")
+        _want(jerk, (3, self.n_loc), "jerk")
+        self._c(lib().nbody_get_derivs(self._ctx, _ptr(acc), _ptr(jerk)))
+        return acc, jerk
+
+    def set_derivs(self, acc, jerk=None):
+        """Restore saved derivatives (exact resume; jerk unused by leapfrog)."""
+        _want(acc, (3, self.n_loc), "acc")
+        _want(jerk, (3, self.n_loc), "jerk")
+        self._c(lib().nbody_set_derivs(self._ctx, _ptr(acc), _ptr(jerk)))
+
+    def set_levels(self, level):
+        """Block time steps: restore saved levels, int32 (n_loc,)."""
+        lev = np.ascontiguousarray(level, dtype=np.int32)
+        if lev.shape != (self.n_loc,):
+            raise ValueError(f"level must have shape ({self.n_loc},), got {lev.shape}")
+        self._c(lib().nbody_set_levels(self._ctx, lev.ctypes.data))
 
     def sync(self):
         self._c(lib().nbody_sync(self._ctx))

@@ -218,6 +218,18 @@ __global__ void validate_kernel(StateArgs a, unsigned long long* bad2) {
     }
 }
 
+__global__ void validate_derivs_kernel(StateArgs a, unsigned long long* bad2) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < a.n_loc; i += gridDim.x * blockDim.x) {
+        bool ok = true;
+        for (int c = 0; c < 3; ++c)
+            ok = ok && isfinite(a.a0[c * a.n_loc_pad + i]) && (a.ncomp != 6 || isfinite(a.j0[c * a.n_loc_pad + i]));
+        if (!ok) flag_bad(&bad2[1], a.i_base + i);
+    }
+}
+__global__ void validate_levels_kernel(StateArgs a, unsigned long long* bad2) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < a.n_loc; i += gridDim.x * blockDim.x)
+        if (a.lev[i] < 0 || a.lev[i] > a.kmax) flag_bad(&bad2[1], a.i_base + i);
+}
 
 // ---------------------------------------------------------------- block time steps
 // NBODY_HERMITE4_BLOCK (NEXT f4, R#28): individual steps
@@ -542,6 +554,16 @@ Dims dims_for(int64_t n) {
 cudaError_t launch_validate(const StateArgs& a, unsigned long long* bad2, cudaStream_t s) {
     if (a.n_loc <= 0) return cudaSuccess;
     validate_kernel<<<dims_for(a.n_loc).grid, dims_for(a.n_loc).block, 0, s>>>(a, bad2);
+    return cudaGetLastError();
+}
+cudaError_t launch_validate_derivs(const StateArgs& a, unsigned long long* bad2, cudaStream_t s) {
+    if (a.n_loc <= 0) return cudaSuccess;
+    validate_derivs_kernel<<<dims_for(a.n_loc).grid, dims_for(a.n_loc).block, 0, s>>>(a, bad2);
+    return cudaGetLastError();
+}
+cudaError_t launch_validate_levels(const StateArgs& a, unsigned long long* bad2, cudaStream_t s) {
+    if (a.n_loc <= 0) return cudaSuccess;
+    validate_levels_kernel<<<dims_for(a.n_loc).grid, dims_for(a.n_loc).block, 0, s>>>(a, bad2);
     return cudaGetLastError();
 }
 cudaError_t launch_pack_state(const StateArgs& a, cudaStream_t s) {

@@ -151,6 +151,9 @@ cudaError_t launch_fill_padding(JPkt* pkt, float4* pklo, JPkt64* pk64, int64_t f
                                 float eps2, cudaStream_t s);
 // bad2[0]: min global index with m not finite or <= 0; bad2[1]: x or v not finite
 cudaError_t launch_validate(const StateArgs& a, unsigned long long* bad2, cudaStream_t s);
+// checkpoint restore: a0, j0 finite (bad2[1] = first bad global index); levels in [0, kmax]
+cudaError_t launch_validate_derivs(const StateArgs& a, unsigned long long* bad2, cudaStream_t s);
+cudaError_t launch_validate_levels(const StateArgs& a, unsigned long long* bad2, cudaStream_t s);
 
 // fp64 energy (energy.cu).  eall: [L] (x, y, z, m) of every particle.
 cudaError_t launch_energy_pack(const StateArgs& a, double4* eall, cudaStream_t s);

@@ -411,13 +411,14 @@ int check_flags(nbody_ctx* c) {
 
 // copy the local [3][n_loc_pad] rows of every shard to/from a user
 // [3][k] array (k = local count, or n in loopback mode)
-int copy_rows(nbody_ctx* c, double* user, bool to_user, bool which_v, bool* host) {
+enum Rows { ROWS_X, ROWS_V, ROWS_A0, ROWS_J0 };
+int copy_rows(nbody_ctx* c, double* user, bool to_user, Rows which, bool* host) {
     int64_t k0 = c->sh.front().plan.i0;
     int64_t k = c->sh.back().plan.i1 - k0;
     *host = !is_device_ptr(user);
     for (auto& s : c->sh) {
         if (s.n_loc <= 0) continue;
-        double* dev = which_v ? s.v : s.x;
+        double* dev = which == ROWS_X ? s.x : which == ROWS_V ? s.v : which == ROWS_A0 ? s.a0 : s.j0;
         double* u = user + (s.plan.i0 - k0);
         if (to_user)
             CK(c, cudaMemcpy2DAsync(u, k * 8, dev, s.n_loc_pad * 8, s.n_loc * 8, 3, cudaMemcpyDefault,
@@ -977,8 +978,8 @@ int nbody_get_state(nbody_ctx* c, double* x, double* v) {
     GUARD(c);
     int rc;
     bool hx = false, hv = false;
-    if (x && (rc = copy_rows(c, x, true, false, &hx))) return rc;
-    if (v && (rc = copy_rows(c, v, true, true, &hv))) return rc;
+    if (x && (rc = copy_rows(c, x, true, ROWS_X, &hx))) return rc;
+    if (v && (rc = copy_rows(c, v, true, ROWS_V, &hv))) return rc;
     if (hx || hv) return check_flags(c);
     return NBODY_OK;
 }
@@ -987,8 +988,8 @@ int nbody_set_state(nbody_ctx* c, const double* x, const double* v, int32_t keep
     GUARD(c);
     int rc;
     bool hx = false, hv = false;
-    if (x && (rc = copy_rows(c, const_cast<double*>(x), false, false, &hx))) return rc;
-    if (v && (rc = copy_rows(c, const_cast<double*>(v), false, true, &hv))) return rc;
+    if (x && (rc = copy_rows(c, const_cast<double*>(x), false, ROWS_X, &hx))) return rc;
+    if (v && (rc = copy_rows(c, const_cast<double*>(v), false, ROWS_V, &hv))) return rc;
     CK(c, cudaMemsetAsync(c->flags + 2, 0xff, 2 * sizeof(unsigned long long), c->stream));
     for (auto& s : c->sh) {
         CK(c, nb::launch_validate(state_args(c, s), c->flags + 2, c->stream));
@@ -1007,6 +1008,68 @@ int nbody_set_state(nbody_ctx* c, const double* x, const double* v, int32_t keep
         c->levels_ok = false;   // block steps: levels restart from eta_s
     }
     c->predicted = false;
+    return NBODY_OK;
+}
+
+int nbody_get_derivs(nbody_ctx* c, double* acc, double* jerk) {
+    GUARD(c);
+    int rc;
+    if ((rc = ensure_forces(c))) return rc;
+    bool ha = false, hj = false;
+    if (acc && (rc = copy_rows(c, acc, true, ROWS_A0, &ha))) return rc;
+    if (jerk && ncomp(c) == 6 && (rc = copy_rows(c, jerk, true, ROWS_J0, &hj))) return rc;
+    if (ha || hj) return check_flags(c);
+    return NBODY_OK;
+}
+
+int nbody_set_derivs(nbody_ctx* c, const double* acc, const double* jerk) {
+    GUARD(c);
+    int rc;
+    if (!acc || (ncomp(c) == 6 && !jerk))
+        return fail(c, NBODY_EINVAL, "acc (and jerk for the Hermite integrators) must be non-NULL");
+    bool ha = false, hj = false;
+    if ((rc = copy_rows(c, const_cast<double*>(acc), false, ROWS_A0, &ha))) return rc;
+    if (ncomp(c) == 6 && (rc = copy_rows(c, const_cast<double*>(jerk), false, ROWS_J0, &hj))) return rc;
+    CK(c, cudaMemsetAsync(c->flags + 2, 0xff, 2 * sizeof(unsigned long long), c->stream));
+    for (auto& s : c->sh) {
+        CK(c, nb::launch_validate_derivs(state_args(c, s), c->flags + 2, c->stream));
+        c->n_kernels++;
+    }
+    unsigned long long bad[2];
+    CK(c, cudaMemcpyAsync(bad, c->flags + 2, sizeof bad, cudaMemcpyDeviceToHost, c->stream));
+    CK(c, cudaStreamSynchronize(c->stream));
+    if (bad[1] != ULLONG_MAX) {
+        c->have_a0 = false;
+        c->predicted = false;
+        return fail(c, NBODY_EINVAL, "acceleration or jerk of particle %llu is not finite", bad[1]);
+    }
+    c->have_a0 = true;      // the next step starts from these derivatives
+    c->predicted = false;
+    return NBODY_OK;
+}
+
+int nbody_set_levels(nbody_ctx* c, const int32_t* level) {
+    GUARD(c);
+    if (!is_block(c)) return fail(c, NBODY_EINVAL, "nbody_set_levels needs NBODY_HERMITE4_BLOCK");
+    if (!level) return fail(c, NBODY_EINVAL, "level must be non-NULL");
+    const int64_t k0 = c->sh.front().plan.i0;
+    for (auto& s : c->sh)
+        if (s.n_loc > 0)
+            CK(c, cudaMemcpyAsync(s.lev, level + (s.plan.i0 - k0), 4 * (size_t)s.n_loc, cudaMemcpyDefault,
+                                  c->stream));
+    CK(c, cudaMemsetAsync(c->flags + 2, 0xff, 2 * sizeof(unsigned long long), c->stream));
+    for (auto& s : c->sh) {
+        CK(c, nb::launch_validate_levels(state_args(c, s), c->flags + 2, c->stream));
+        c->n_kernels++;
+    }
+    unsigned long long bad[2];
+    CK(c, cudaMemcpyAsync(bad, c->flags + 2, sizeof bad, cudaMemcpyDeviceToHost, c->stream));
+    CK(c, cudaStreamSynchronize(c->stream));
+    if (bad[1] != ULLONG_MAX) {
+        c->levels_ok = false;
+        return fail(c, NBODY_EINVAL, "level of particle %llu is outside [0, kmax = %d]", bad[1], c->cfg.kmax);
+    }
+    c->levels_ok = true;    // the next nbody_step keeps them (no eta_s restart)
     return NBODY_OK;
 }
 
