@@ -6,7 +6,11 @@ simulation window with idle padding before/after (5 s instead 
 120 s).  Prints one JSON line; the paper's numbers are quoted as context only
 (other hardware, unknown ICs).
 
-  python scripts/paper_run.py [--repeats 5] [--pad 5]
+  python scripts/paper_run.py [--repeats 5] [--pad 5] [--trace power.csv]
+
+--trace writes the power time series the paper plots: NVML power
+samples every 50 ms over the whole measurement, idle pads included, as CSV
+(seconds since start, device, watts, phase).
 """
 import argparse
 import json
@@ -24,6 +28,7 @@ def main():
     ap.add_argument("--repeats", type=int, default=5)
     ap.add_argument("--pad", type=float, default=5.0)
     ap.add_argument("--integrator", default="hermite")
+    ap.add_argument("--trace", default=None)
     a = ap.parse_args()
     import numpy as np
     import torch
@@ -38,6 +43,27 @@ def main():
         s.step(1)
         s.sync()
     meter = EnergyMeter(0)
+    trace, phase = [], ["idle"]
+    stop = [False]
+
+    def sampler():   # NVML power every 50 ms (the paper samples at ~1 Hz)
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(0)
+        except Exception:
+            return
+        t0 = time.perf_counter()
+        while not stop[0]:
+            try:
+                trace.append((time.perf_counter() - t0, pynvml.nvmlDeviceGetPowerUsage(h) / 1000.0, phase[0]))
+            except Exception:
+                pass
+            time.sleep(0.05)
+
+    import threading
+    th = threading.Thread(target=sampler, daemon=True)
+    th.start()
 
     def simulate():
         t0 = time.perf_counter()
@@ -52,28 +78,41 @@ def main():
     # NVML's energy counter updates too coarsely for a ~0.15 s run: each repeat
     # integrates over a batch of back-to-back simulations (window >= 3 s) and
     # reports the per-simulation mean.
-    t1, _ = simulate()
+    warm = [simulate()[0] for _ in range(3)]   # first calls include one-time set-up
+    t1 = statistics.median(warm)
     batch = max(1, int(3.0 / max(t1, 1e-3)))
     runs = []
     for r in range(a.repeats):
+        phase[0] = "idle"
         time.sleep(a.pad)
+        phase[0] = "run"
         meter.start()
         ts, E = [], None
         for _ in range(batch):
             t, E = simulate()
             ts.append(t)
         e = meter.stop()
+        phase[0] = "idle"
         for t in ts:
             runs.append({"seconds": t, "gpu_joules": (e["gpu_joules"] / batch
                                                       if e["gpu_joules"] is not None else None),
                          "energy_after": E})
         time.sleep(a.pad)
+    stop[0] = True
+    th.join(timeout=1)
+    if a.trace and trace:
+        with open(a.trace, "w") as f:
+            f.write("seconds,device,watts,phase\n")
+            for t, w, ph in trace:
+                f.write(f"{t:.3f},0,{w:.1f},{ph}\n")
+    pw = {ph: [w for _, w, p in trace if p == ph] for ph in ("idle", "run")}
     ts = [r["seconds"] for r in runs]
     es = [r["gpu_joules"] for r in runs if r["gpu_joules"] is not None]
     out = {
         "workload": f"PAPER: Plummer N={c.n} eps={c.eps} dt=1/1024, {c.steps} {a.integrator} steps "
                     "(+ t=0 force evaluation, final state D2H and fp64 energy)",
-        "time_to_solution_s": {"mean": statistics.mean(ts), "stdev": statistics.pstdev(ts),
+        "time_to_solution_s": {"median": statistics.median(ts), "mean": statistics.mean(ts),
+                               "stdev": statistics.pstdev(ts),
                                "min": min(ts), "max": max(ts), "runs": len(ts)},
         "energy_to_solution_j": ({"mean": statistics.mean(es), "stdev": statistics.pstdev(es),
                                   "runs": len(es), "scope": "1 GPU, NVML total-energy counter"}
@@ -85,6 +124,8 @@ def main():
             "note": "paper ICs, softening, dt and 'time cycle' unstated; not comparable targets",
         },
         "energy_batch": batch,
+        "power_w": {ph: ({"mean": statistics.mean(v), "max": max(v), "samples": len(v)} if v else None)
+                    for ph, v in pw.items()},
         "runs": runs[:10],
     }
     print(json.dumps(out))
