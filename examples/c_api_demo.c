@@ -7,7 +7,9 @@
  *
  * Builds a seeded uniform-cube system in host memory, lets nbody_init copy it to the GPU,
  * evaluates forces into host arrays (nbody_compute_forces), advances 10 Hermite steps
- * (nbody_step) and prints the energy before and after (nbody_energy).
+ * (nbody_step) and prints the energy before and after (nbody_energy); then checkpoints
+ * (nbody_get_state + nbody_get_derivs), resumes in a second context (nbody_init +
+ * nbody_set_derivs) and checks that 5 more steps in both contexts agree bit for bit.
  */
 #include <math.h>
 #include <stdint.h>
@@ -80,7 +82,28 @@ int main(int argc, char** argv) {
            py, pz);
     printf("E0 = %.12f  E(10 dt) = %.12f  rel. change %.2e\n", ke0 + pe0, ke1 + pe1,
            fabs((ke1 + pe1) - (ke0 + pe0)) / fabs(ke0 + pe0));
+    /* checkpoint at this call boundary, resume in a fresh context, 5 more steps in both */
+    double* x2 = malloc(sizeof(double) * 3 * n);
+    double* v2 = malloc(sizeof(double) * 3 * n);
+    nbody_ctx* ctx2 = NULL;
+    rc = nbody_get_derivs(ctx, acc, jerk);
+    if (!rc) rc = nbody_init(&cfg, m, x, v, &ctx2);
+    if (!rc) rc = nbody_set_derivs(ctx2, acc, jerk);
+    if (!rc) rc = nbody_step(ctx, 5);
+    if (!rc) rc = nbody_step(ctx2, 5);
+    if (!rc) rc = nbody_get_state(ctx, x, v);
+    if (!rc) rc = nbody_get_state(ctx2, x2, v2);
+    if (rc) {
+        fprintf(stderr, "resume error %d: %s\n", rc, nbody_last_error(ctx2 ? ctx2 : ctx));
+        nbody_destroy(ctx2);
+        nbody_destroy(ctx);
+        return 1;
+    }
+    int same = 1;
+    for (int64_t k = 0; k < 3 * n; ++k) same &= x[k] == x2[k] && v[k] == v2[k];
+    printf("resume: %s\n", same ? "bit-identical" : "DIFFERS");
+    nbody_destroy(ctx2);
     nbody_destroy(ctx);
-    free(m); free(x); free(v); free(acc); free(jerk);
-    return 0;
+    free(m); free(x); free(v); free(acc); free(jerk); free(x2); free(v2);
+    return same ? 0 : 1;
 }

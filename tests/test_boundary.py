@@ -156,10 +156,12 @@ def test_c_program_links_against_the_c_abi(tmp_path):
 
 @pytest.mark.gpu
 def test_c_program_runs_the_hot_path(tmp_path):
-    """The same C program on the GPU: forces into host arrays, 10 Hermite steps, energy."""
+    """The same C program on the GPU: forces into host arrays, 10 Hermite steps, energy,
+    then checkpoint / resume in a second context, bit-identical after 5 more steps."""
     import re
     import subprocess
     exe = _build_c_demo(tmp_path)
     out = subprocess.run([str(exe), "4096"], capture_output=True, text=True, check=True).stdout
     rel = float(re.search(r"rel\. change ([0-9.e+-]+)", out).group(1))
     assert rel < 1e-6, out
+    assert "resume: bit-identical" in out, out
