@@ -372,7 +372,8 @@ __global__ void block_decide_kernel(long long* ctl, const unsigned long long* tn
 __device__ __forceinline__ void select_predict_one(const StateArgs& a, int i, unsigned long long tn,
                                                    double tick, int32_t* nact) {
     NB_CHECK((unsigned long long)(a.T[i] + ticks_of(a, a.lev[i])) >= tn);   // none left behind
-    if ((unsigned long long)(a.T[i] + ticks_of(a, a.lev[i])) == tn) {
+    const bool active = (unsigned long long)(a.T[i] + ticks_of(a, a.lev[i])) == tn;
+    if (active) {
         const int slot = atomicAdd(nact, 1);
         NB_CHECK(slot >= 0 && slot < a.n_loc);
         a.ilist[slot] = i;
@@ -390,8 +391,10 @@ __device__ __forceinline__ void select_predict_one(const StateArgs& a, int i, un
         const double x = xs[c], v = vs[c], ac = as[c], jk = js[c];
         xp[c] = x + v * D + ac * D2 / 2.0 + jk * D3 / 6.0;
         vp[c] = v + ac * D + jk * D2 / 2.0;
-        a.xp[o] = xp[c];
-        a.vp[o] = vp[c];
+        if (active) {   // only the corrector reads xp, vp, and only for active particles
+            a.xp[o] = xp[c];
+            a.vp[o] = vp[c];
+        }
         ok = ok && isfinite(xp[c]) && isfinite(vp[c]);
     }
     if (!ok) flag_bad(a.bad, a.i_base + i);
