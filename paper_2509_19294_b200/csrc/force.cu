@@ -110,7 +110,17 @@ struct FkCfg {
     static constexpr int kSmemBytes = kOffAcc + kAccSmemBytes;
 };
 using CfgBig = FkCfg<FK_PAIRS, FK_THREADS, FK_MINB, FK_MINB_ACC, FK_HYB>;
-using CfgSmall = FkCfg<1, 128, 6, 6, 0, FK_SMALL_UNROLL, FK_SMALL_LIST_UNROLL>;
+#ifndef FK_SMALL_PAIRS
+#define FK_SMALL_PAIRS 1
+#endif
+#ifndef FK_SMALL_THREADS
+#define FK_SMALL_THREADS 128
+#endif
+#ifndef FK_SMALL_MINB
+#define FK_SMALL_MINB 6
+#endif
+using CfgSmall = FkCfg<FK_SMALL_PAIRS, FK_SMALL_THREADS, FK_SMALL_MINB, FK_SMALL_MINB, 0, FK_SMALL_UNROLL,
+                       FK_SMALL_LIST_UNROLL>;
 constexpr int kIPerBlock = CfgBig::kIPerBlock;
 constexpr int kHyb = CfgBig::kHyb;
 
