@@ -298,11 +298,15 @@ __global__ void block_reset_time_kernel(StateArgs a) {
 // t_next = min_i (t_i + dt_i): exact integer minimum, so order-independent;
 // one atomic per warp after a shuffle reduction
 
-__global__ void block_begin_kernel(unsigned long long* tnext, int32_t* nact, int nshards,
-                                   const int32_t* lvl_cnt, int kmax) {
-    const unsigned long long t0 = next_block_time(lvl_cnt, kmax, 0);   // 32 threads
-    if (threadIdx.x == 0) *tnext = t0;
+__global__ void block_begin_kernel(unsigned long long* tcur, int32_t* nact, int nshards) {
+    if (threadIdx.x == 0) *tcur = 0;
     for (int q = threadIdx.x; q < nshards; q += blockDim.x) nact[q] = 0;
+}
+
+// NCCL ranks: the rank's own t_next (one warp), reduced with MIN over ranks afterwards
+__global__ void block_tnext_kernel(StateArgs a) {
+    const unsigned long long tn = next_block_time(a.lvl_cnt, a.kmax, *a.tcur);
+    if (threadIdx.x == 0) *a.tnext = tn;
 }
 
 __global__ void block_set_tend_kernel(long long* ctl, unsigned long long t_end) {
@@ -317,19 +321,25 @@ __device__ __forceinline__ cudaGraphDeviceNode_t force_node(const BlockGraphNode
                                                                            : nodes->force_big[q];
 }
 
-__global__ void block_decide_kernel(long long* ctl, const unsigned long long* tnext, int32_t* nact,
+__global__ void block_decide_kernel(long long* ctl, const unsigned long long* tnext,
+                                    unsigned long long* tcur, int32_t* append, int32_t* nact,
                                     int nshards, cudaGraphConditionalHandle cond,
                                     BlockGraphNodes* nodes) {
     const bool done = *tnext > (unsigned long long)ctl[0];
-    if (done) {
-        for (int q = 0; q < nshards; ++q) nact[q] = 0;
-    } else {
-        long long na = 0;
-        for (int q = 0; q < nshards; ++q) na += nact[q];
+    // freeze this block step's active counts (force passes and corrector read them) and
+    // reset the selection pass's append counters for the next block step
+    long long na = 0;
+    for (int q = 0; q < nshards; ++q) {
+        nact[q] = done ? 0 : append[q];
+        append[q] = 0;
+        na += nact[q];
+    }
+    if (!done) {
         ctl[1] += 1;
         ctl[2] += na;
     }
     ctl[3] = done ? 1 : 0;
+    *tcur = *tnext;   // the clock the next selection pass starts from
     if (nodes) {   // inside the block-step graph
         for (int q = 0; q < nshards; ++q) {
             if (!nodes->force[q]) continue;   // shard without particles: no force node
@@ -402,7 +412,22 @@ __device__ __forceinline__ void select_predict_one(const StateArgs& a, int i, un
 }
 
 __global__ void block_select_predict_kernel(StateArgs a) {
-    const unsigned long long tn = *a.tnext;
+    // t_next: from the level counts the previous corrector left (every CTA derives the same
+    // value; CTA 0 publishes it for decide / force / corrector), or given (NCCL ranks)
+    __shared__ unsigned long long tn_s;
+    if (a.self_tnext) {
+        if (threadIdx.x < 32) {
+            const unsigned long long t = next_block_time(a.lvl_cnt, a.kmax, *a.tcur);
+            if (threadIdx.x == 0) {
+                tn_s = t;
+                if (blockIdx.x == 0) *a.tnext = t;
+            }
+        }
+    } else if (threadIdx.x == 0) {
+        tn_s = *a.tnext;
+    }
+    __syncthreads();
+    const unsigned long long tn = tn_s;
     const double tick = ldexp(a.dt, -a.kmax);
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < a.n_loc; i += gridDim.x * blockDim.x)
         select_predict_one(a, i, tn, tick, a.nact);
@@ -487,8 +512,8 @@ __device__ __forceinline__ void correct_slot(const StateArgs& a, int i, const Co
 // (bandwidth-bound); the results are identical.
 constexpr int kWarpFoldMax = 4096;
 
-__global__ void block_correct_kernel(StateArgs a, int32_t* reset_nact, int reset_n, int32_t* done_ctas) {
-    const int32_t n_act = *a.nact;
+__global__ void block_correct_kernel(StateArgs a) {
+    const int32_t n_act = *a.nact_cur;
     const unsigned long long tn = *a.tnext;
     const int nw = (int)((gridDim.x * blockDim.x) >> 5);
     if (n_act <= min(kWarpFoldMax, nw) && a.ncomp == 6) {   // at most one slot per warp
@@ -511,27 +536,6 @@ __global__ void block_correct_kernel(StateArgs a, int32_t* reset_nact, int reset
             double f[6];
             fold_all(a, q, f);
             correct_slot(a, i, in, f, tn);
-        }
-    }
-    // the last CTA of the last shard's launch resets t_next and the active counts for the
-    // next block step (every CTA has read them by the time it counts itself done)
-    if (reset_nact) {
-        __shared__ int last;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            __threadfence();
-            last = atomicAdd(done_ctas, 1) == (int)gridDim.x - 1;
-        }
-        __syncthreads();
-        if (last && threadIdx.x < 32) {
-            __threadfence();   // every CTA's level updates are visible
-            const unsigned long long nt = next_block_time(a.lvl_cnt, a.kmax, tn);
-            if (threadIdx.x == 0) {
-                *a.tnext = nt;
-                for (int q = 0; q < reset_n; ++q) reset_nact[q] = 0;
-                *done_ctas = 0;
-                __threadfence();
-            }
         }
     }
 }
@@ -607,25 +611,27 @@ cudaError_t launch_block_select_predict(const StateArgs& a, cudaStream_t s) {
     block_select_predict_kernel<<<dims_for(a.n_loc).grid, dims_for(a.n_loc).block, 0, s>>>(a);
     return cudaGetLastError();
 }
-cudaError_t launch_block_correct(const StateArgs& a, int32_t* reset_nact, int reset_n, int32_t* done_ctas,
-                                 cudaStream_t s) {
-    block_correct_kernel<<<dims_for(a.n_loc > 0 ? a.n_loc : 1).grid, dims_for(a.n_loc > 0 ? a.n_loc : 1).block, 0, s>>>(a, reset_nact, reset_n,
-                                                                                   done_ctas);
+cudaError_t launch_block_correct(const StateArgs& a, cudaStream_t s) {
+    block_correct_kernel<<<dims_for(a.n_loc > 0 ? a.n_loc : 1).grid, dims_for(a.n_loc > 0 ? a.n_loc : 1).block, 0,
+                           s>>>(a);
     return cudaGetLastError();
 }
-cudaError_t launch_block_begin(unsigned long long* tnext, int32_t* nact, int nshards,
-                               const int32_t* lvl_cnt, int kmax, cudaStream_t s) {
-    block_begin_kernel<<<1, 32, 0, s>>>(tnext, nact, nshards, lvl_cnt, kmax);
+cudaError_t launch_block_begin(unsigned long long* tcur, int32_t* nact, int nshards, cudaStream_t s) {
+    block_begin_kernel<<<1, 32, 0, s>>>(tcur, nact, nshards);
+    return cudaGetLastError();
+}
+cudaError_t launch_block_tnext(const StateArgs& a, cudaStream_t s) {
+    block_tnext_kernel<<<1, 32, 0, s>>>(a);
     return cudaGetLastError();
 }
 cudaError_t launch_block_set_tend(long long* ctl, unsigned long long t_end, cudaStream_t s) {
     block_set_tend_kernel<<<1, 1, 0, s>>>(ctl, t_end);
     return cudaGetLastError();
 }
-cudaError_t launch_block_decide(long long* ctl, const unsigned long long* tnext, int32_t* nact,
-                                int nshards, cudaGraphConditionalHandle cond,
-                                BlockGraphNodes* nodes, cudaStream_t s) {
-    block_decide_kernel<<<1, 1, 0, s>>>(ctl, tnext, nact, nshards, cond, nodes);
+cudaError_t launch_block_decide(long long* ctl, const unsigned long long* tnext, unsigned long long* tcur,
+                                int32_t* nact, int32_t* nact_cur, int nshards,
+                                cudaGraphConditionalHandle cond, BlockGraphNodes* nodes, cudaStream_t s) {
+    block_decide_kernel<<<1, 1, 0, s>>>(ctl, tnext, tcur, nact, nact_cur, nshards, cond, nodes);
     return cudaGetLastError();
 }
 cudaError_t launch_fill_padding(JPkt* pkt, float4* pklo, JPkt64* pk64, int64_t from, int64_t to,

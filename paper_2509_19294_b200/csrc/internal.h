@@ -136,8 +136,12 @@ struct StateArgs {
     int64_t* T;          // [n_loc] particle time in ticks of dt_max / 2^kmax
     int32_t* lev;        // [n_loc] level k: dt_i = dt_max / 2^k
     int32_t* ilist;      // [n_loc] active particles (local indices), slot order
-    int32_t* nact;       // active count (device counter)
-    unsigned long long* tnext;  // next block time in ticks (device, shared by shards)
+    int32_t* nact;       // active-set append counter of the selection pass (device)
+    int32_t* nact_cur;   // this block step's active count, frozen by the decide kernel
+    unsigned long long* tnext;  // this block step's time in ticks (device, shared by shards)
+    unsigned long long* tcur;   // the previous block step's time (the clock the levels refer to)
+    int32_t self_tnext;  // 1: the selection pass derives t_next from the level counts itself;
+                         // 0: t_next is already in *tnext (NCCL ranks: a min over ranks)
     int32_t* lvl_cnt;    // [64] particles per level, all shards (device); t_next derives from it
     long long* ctl;      // block-run control [t_end ticks, block steps, sum of active, done]
     int32_t kmax;
@@ -167,10 +171,10 @@ int energy_blocks(int32_t n_loc);
 // Both add every local particle's level to lvl_cnt (zeroed by the caller first).
 cudaError_t launch_block_init_levels(const StateArgs& a, cudaStream_t s);  // lev from eta_s, T = 0
 cudaError_t launch_block_reset_time(const StateArgs& a, cudaStream_t s);   // T = 0 (call start)
-// first t_next of a call (clock at 0) from the level counts; active counts of all nshards
-// shards reset.  Later t_next values come from the corrector's last CTA (same rule).
-cudaError_t launch_block_begin(unsigned long long* tnext, int32_t* nact, int nshards,
-                               const int32_t* lvl_cnt, int kmax, cudaStream_t s);
+// start of a call: clock at 0 (tcur), append counters of all nshards shards reset
+cudaError_t launch_block_begin(unsigned long long* tcur, int32_t* nact, int nshards, cudaStream_t s);
+// NCCL ranks: this rank's t_next from its level counts into *tnext (then a min over ranks)
+cudaError_t launch_block_tnext(const StateArgs& a, cudaStream_t s);
 // ctl[0] = t_end (start of a call)
 cudaError_t launch_block_set_tend(long long* ctl, unsigned long long t_end, cudaStream_t s);
 // after t_next and the active sets: done = t_next > t_end (then the active counts are zeroed so
@@ -189,16 +193,15 @@ struct BlockGraphNodes {
     int32_t ts_max, ts1_max;             // active counts <= ts1_max: scalar; <= ts_max: packed
     int32_t cur[8];                      // enabled force node per shard (kind, -1 none, -2 unknown)
 };
-cudaError_t launch_block_decide(long long* ctl, const unsigned long long* tnext, int32_t* nact,
-                                int nshards, cudaGraphConditionalHandle cond,
-                                BlockGraphNodes* nodes, cudaStream_t s);
+cudaError_t launch_block_decide(long long* ctl, const unsigned long long* tnext, unsigned long long* tcur,
+                                int32_t* nact, int32_t* nact_cur, int nshards,
+                                cudaGraphConditionalHandle cond, BlockGraphNodes* nodes, cudaStream_t s);
 
 // active set + every particle predicted to t_next and packed (one pass)
 cudaError_t launch_block_select_predict(const StateArgs& a, cudaStream_t s);
-// correct the active particles (count read on the device), new levels, T = t_next; with
-// reset_nact != nullptr its last CTA resets t_next and reset_nact[0 .. reset_n) for the next
-// block step (done_ctas: zero-initialised CTA counter)
-cudaError_t launch_block_correct(const StateArgs& a, int32_t* reset_nact, int reset_n, int32_t* done_ctas,
-                                 cudaStream_t s);
+// correct the active particles (count nact_cur, read on the device), new levels and level
+// counts, T = t_next.  No grid-wide tail: the next selection pass derives its t_next from
+// the level counts and the decide kernel resets the append counters.
+cudaError_t launch_block_correct(const StateArgs& a, cudaStream_t s);
 
 }  // namespace nb

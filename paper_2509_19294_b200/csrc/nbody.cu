@@ -156,11 +156,12 @@ struct nbody_ctx {
     unsigned long long* flags = nullptr;  // [0] non-finite, [1] coincident, [2..3] validate
     // block time steps (R#28): t_next (ticks, shared by all shards), per-shard
     // active counts, pinned read-back of both, run statistics
-    unsigned long long* tnext = nullptr;
-    int32_t* nact = nullptr;
+    unsigned long long* tnext = nullptr;   // this block step's time (ticks)
+    unsigned long long* tcur = nullptr;    // the previous block step's time
+    int32_t* nact = nullptr;               // per shard: selection append counters
+    int32_t* nact_cur = nullptr;           // per shard: this block step's active counts
     int32_t* lvl_cnt = nullptr;   // [64] particles per level, all shards
     nb::BlockGraphNodes* gnodes = nullptr;   // device copy of the graph's force-node handles
-    int32_t* done_ctas = nullptr;            // last-CTA counter of the correct kernel
     long long* ctl = nullptr;            // [t_end, block steps, active sum, done] (device)
     void* hbuf = nullptr;
     bool levels_ok = false;
@@ -249,7 +250,10 @@ nb::StateArgs state_args(nbody_ctx* c, Shard& s) {
     a.lev = s.lev;
     a.ilist = s.ilist;
     a.nact = c->nact ? c->nact + (&s - c->sh.data()) : nullptr;
+    a.nact_cur = c->nact_cur ? c->nact_cur + (&s - c->sh.data()) : nullptr;
     a.tnext = c->tnext;
+    a.tcur = c->tcur;
+    a.self_tnext = c->comm ? 0 : 1;   // NCCL ranks reduce t_next over ranks first
     a.lvl_cnt = c->lvl_cnt;
     a.ctl = c->ctl;
     a.kmax = c->cfg.kmax;
@@ -442,11 +446,12 @@ void free_ctx(nbody_ctx* c) {
         cudaFree(s.T); cudaFree(s.lev); cudaFree(s.ilist);
     }
     cudaFree(c->tnext);
+    cudaFree(c->tcur);
+    cudaFree(c->nact_cur);
     cudaFree(c->nact);
     cudaFree(c->lvl_cnt);
     cudaFree(c->ctl);
     cudaFree(c->gnodes);
-    cudaFree(c->done_ctas);
     if (c->block_graph) cudaGraphExecDestroy(c->block_graph);
     if (c->hbuf) cudaFreeHost(c->hbuf);
     cudaFree(c->pkt);
@@ -530,13 +535,12 @@ int init_impl(const nbody_config* cfg, const double* m, const double* x, const d
     if (nb::force_hyb() > 0 && (rc = dalloc(c, &c->pk64, (size_t)c->L))) return rc;
     if ((rc = dalloc(c, &c->flags, 4))) return rc;
     if (is_block(c)) {
-        if ((rc = dalloc(c, &c->tnext, 1)) || (rc = dalloc(c, &c->nact, (size_t)c->nshards)) ||
+        if ((rc = dalloc(c, &c->tnext, 1)) || (rc = dalloc(c, &c->tcur, 1)) ||
+            (rc = dalloc(c, &c->nact, (size_t)c->nshards)) || (rc = dalloc(c, &c->nact_cur, (size_t)c->nshards)) ||
             (rc = dalloc(c, &c->lvl_cnt, 64)) ||
-            (rc = dalloc(c, &c->ctl, 4)) || (rc = dalloc(c, &c->gnodes, 1)) ||
-            (rc = dalloc(c, &c->done_ctas, 1)))
+            (rc = dalloc(c, &c->ctl, 4)) || (rc = dalloc(c, &c->gnodes, 1)))
             return rc;
         CK(c, cudaMemsetAsync(c->ctl, 0, 4 * sizeof(long long), c->stream));
-        CK(c, cudaMemsetAsync(c->done_ctas, 0, sizeof(int32_t), c->stream));
         CK(c, cudaMallocHost(&c->hbuf, 8 + 4 * (size_t)c->nshards));
     }
     CK(c, cudaMemsetAsync(c->flags, 0xff, 4 * sizeof(unsigned long long), c->stream));
@@ -694,12 +698,15 @@ namespace {
 // the last CTA of each block step's corrector)
 int block_step_body(nbody_ctx* c, cudaGraphConditionalHandle cond, nb::BlockGraphNodes* nodes) {
     int rc;
-    // t_next of this block step was set by the previous step's corrector (or block_begin)
-    // from the level counts; with NCCL ranks it is the minimum over the ranks
-    if (use_nccl(c))
+    // t_next from the level counts the previous corrector left: derived by the selection
+    // pass itself, except with NCCL ranks, where it is each rank's value reduced with MIN
+    if (use_nccl(c)) {
+        CK(c, nb::launch_block_tnext(state_args(c, c->sh[0]), c->stream));
         CKNCCL(c, nccl().AllReduce(c->tnext, c->tnext, 1, ncclUint64, ncclMin, c->comm, c->stream));
+    }
     for (auto& s : c->sh) CK(c, nb::launch_block_select_predict(state_args(c, s), c->stream));
-    CK(c, nb::launch_block_decide(c->ctl, c->tnext, c->nact, c->nshards, cond, nodes, c->stream));
+    CK(c, nb::launch_block_decide(c->ctl, c->tnext, c->tcur, c->nact, c->nact_cur, c->nshards, cond, nodes,
+                                  c->stream));
     return NBODY_OK;
 }
 
@@ -756,14 +763,14 @@ int block_step_rest(nbody_ctx* c, const int32_t* n_act, nb::BlockGraphNodes* nod
         if (n_i <= 0 || s.n_loc <= 0) continue;
         const int32_t nch = (int32_t)s.plan.n_chunks;
         if (nodes) {
-            if ((rc = launch_force_range(c, s, 0, nch, n_i, s.ilist, c->nact + q)) ||
+            if ((rc = launch_force_range(c, s, 0, nch, n_i, s.ilist, c->nact_cur + q)) ||
                 (rc = capture_force_node(c, &nodes->force[q])))
                 return rc;
             // the 1024-i list node only where an active set can reach big_min (a disabled
             // node still costs the graph a little every block step)
             nodes->big_min[q] = list_big_min(c, s);
             if (nodes->big_min[q] <= s.n_loc) {
-                if ((rc = launch_force_range(c, s, 0, nch, n_i, s.ilist, c->nact + q, 3)) ||
+                if ((rc = launch_force_range(c, s, 0, nch, n_i, s.ilist, c->nact_cur + q, 3)) ||
                     (rc = capture_force_node(c, &nodes->force_big[q])))
                     return rc;
             } else {
@@ -772,22 +779,18 @@ int block_step_rest(nbody_ctx* c, const int32_t* n_act, nb::BlockGraphNodes* nod
             nodes->chunks[q] = nch;
             nodes->ts_ok[q] = packed_tsplit_ok(s) ? 1 : 0;
             if (nodes->ts_ok[q] &&
-                ((rc = launch_force_range(c, s, 0, nch, n_i, s.ilist, c->nact + q, 1)) ||
+                ((rc = launch_force_range(c, s, 0, nch, n_i, s.ilist, c->nact_cur + q, 1)) ||
                  (rc = capture_force_node(c, &nodes->force_ts[q]))))
                 return rc;
             if (nodes->ts1_max > 0 &&
-                ((rc = launch_force_range(c, s, 0, nch, n_i, s.ilist, c->nact + q, 2)) ||
+                ((rc = launch_force_range(c, s, 0, nch, n_i, s.ilist, c->nact_cur + q, 2)) ||
                  (rc = capture_force_node(c, &nodes->force_ts1[q]))))
                 return rc;
-        } else if ((rc = launch_force_range(c, s, 0, nch, n_i, s.ilist, c->nact + q, block_force_kind(c, s, n_i)))) {
+        } else if ((rc = launch_force_range(c, s, 0, nch, n_i, s.ilist, c->nact_cur + q, block_force_kind(c, s, n_i)))) {
             return rc;
         }
     }
-    for (int q = 0; q < c->nshards; ++q) {
-        const bool last = q == c->nshards - 1;
-        CK(c, nb::launch_block_correct(state_args(c, c->sh[q]), last ? c->nact : nullptr, c->nshards,
-                                       c->done_ctas, c->stream));
-    }
+    for (int q = 0; q < c->nshards; ++q) CK(c, nb::launch_block_correct(state_args(c, c->sh[q]), c->stream));
     c->n_kernels += 1 + 3 * (int64_t)c->nshards;   // select, force, correct; decide
     return NBODY_OK;
 }
@@ -808,7 +811,7 @@ int block_run(nbody_ctx* c, int32_t nsteps) {
     }
     c->levels_ok = true;
     CK(c, nb::launch_block_set_tend(c->ctl, (unsigned long long)nsteps << kmax, c->stream));
-    CK(c, nb::launch_block_begin(c->tnext, c->nact, c->nshards, c->lvl_cnt, kmax, c->stream));
+    CK(c, nb::launch_block_begin(c->tcur, c->nact, c->nshards, c->stream));
     const bool graph_ok = !use_nccl(c) && !c->prof && c->use_graph && c->nshards <= 8 &&
                           c->stream != cudaStreamLegacy && c->stream != cudaStreamPerThread &&
                           c->stream != nullptr;
@@ -870,7 +873,7 @@ int block_run(nbody_ctx* c, int32_t nsteps) {
     for (;;) {
         if ((rc = block_step_body(c, cudaGraphConditionalHandle{}, nullptr))) return rc;
         CK(c, cudaMemcpyAsync(h_done, c->ctl + 3, sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
-        CK(c, cudaMemcpyAsync(h_nact, c->nact, 4 * (size_t)c->nshards, cudaMemcpyDeviceToHost, c->stream));
+        CK(c, cudaMemcpyAsync(h_nact, c->nact_cur, 4 * (size_t)c->nshards, cudaMemcpyDeviceToHost, c->stream));
         CK(c, cudaStreamSynchronize(c->stream));
         if (*h_done) break;
         if ((rc = block_step_rest(c, h_nact, nullptr))) return rc;
