@@ -1,6 +1,8 @@
 """Randomised GPU parity sweep through the C-ABI: seeded random system sizes, softenings,
 shard counts, position modes and integrators, each checked against the fp64 oracle and
 against the unsharded run.  The seeds are fixed, so a failure is reproducible."""
+import os
+
 import numpy as np
 import pytest
 
@@ -11,7 +13,8 @@ from metrics import TOL_ACC, TOL_JERK, max_rel
 pytestmark = pytest.mark.gpu
 torch = pytest.importorskip("torch")
 
-CASES = list(range(24))
+# NBODY_FUZZ_CASES=k widens both sweeps for an occasional deep run (default 24 / 12)
+CASES = list(range(int(os.environ.get("NBODY_FUZZ_CASES", "24"))))
 
 
 def _case(k):
@@ -52,7 +55,7 @@ def test_random_case(k):
     assert all(np.isfinite(t).all() for t in out[1])
 
 
-BLOCK_CASES = list(range(12))
+BLOCK_CASES = list(range(int(os.environ.get("NBODY_FUZZ_CASES", "12"))))
 
 
 @pytest.mark.parametrize("k", BLOCK_CASES)
@@ -98,6 +101,10 @@ def test_random_block_case(k, monkeypatch):
         e2 = float(np.float32(eps * eps))
         xo, vo, _, _, lo, so, co = oracle.hermite_block(m, x, v, e2, dt_max, 1, eta=eta, eta_s=0.01,
                                                         kmax=20)
-        assert abs(ref[3][0] - so[0]) <= 0.05 * so[0] + 2, (k, ref[3], so)
+        # force evaluations are the robust schedule statistic; the block-step count is not
+        # (one particle on the adjacent, also valid, finer level near a boundary adds block
+        # steps with tiny active sets -- see test_block_c4_schedule_and_state_vs_oracle)
+        assert abs(ref[3][1] - so[1]) <= 0.02 * so[1] + 8, (k, ref[3], so)
+        assert ref[3][0] <= 2 * so[0] + 8 and so[0] <= 2 * ref[3][0] + 8, (k, ref[3], so)
         # positions agree to the level of a few adjacent-level choices (see test_gpu_block)
         assert np.max(np.abs(ref[0] - xo)) <= 1e-6, (k, np.max(np.abs(ref[0] - xo)))
