@@ -699,9 +699,19 @@ __global__ void __launch_bounds__(kTsWarpsMax * 32, 2) force_tsplit_kernel(Force
     float* tsum = reinterpret_cast<float*>(smem + C::off_sum(W));
     double* acc64 = reinterpret_cast<double*>(smem + C::off_acc(W));
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + C::off_bar(W)) + w;
+    const int c = (a.c_first + (int)blockIdx.y) % a.n_chunks;
+    const int64_t jc0 = (int64_t)c * a.chunk;
+    const int ntile = a.chunk / kTile;
+    // stage tile t with one bulk TMA copy (+ the hi/lo tails) on the warp's mbarrier
+    auto stage = [&](int t) {
+        mbar_expect_tx(bar, kTileBytes + (kHiLo ? kLoTileBytes : 0));
+        tma_load_1d(tile, a.pkt + jc0 + (int64_t)t * kTile, kTileBytes, bar);
+        if (kHiLo) tma_load_1d(tile_lo, a.pklo + jc0 + (int64_t)t * kTile, kLoTileBytes, bar);
+    };
     if (lane == 0) {
         mbar_init(bar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        if (w < ntile) stage(w);   // first tile in flight while the i-particles load
     }
     __syncwarp();
 
@@ -734,19 +744,11 @@ __global__ void __launch_bounds__(kTsWarpsMax * 32, 2) force_tsplit_kernel(Force
     }
     for (int k = tid; k < kNC * kI; k += blockDim.x) acc64[k] = 0.0;
 
-    const int c = (a.c_first + (int)blockIdx.y) % a.n_chunks;
-    const int64_t jc0 = (int64_t)c * a.chunk;
-    const int ntile = a.chunk / kTile;
     uint32_t phase = 0;
     for (int r0 = 0; r0 < ntile; r0 += W) {
         const int t = r0 + w;
         if (t < ntile) {
-            // stage tile t with one bulk TMA copy (+ the hi/lo tails) on the warp's mbarrier
-            if (lane == 0) {
-                mbar_expect_tx(bar, kTileBytes + (kHiLo ? kLoTileBytes : 0));
-                tma_load_1d(tile, a.pkt + jc0 + (int64_t)t * kTile, kTileBytes, bar);
-                if (kHiLo) tma_load_1d(tile_lo, a.pklo + jc0 + (int64_t)t * kTile, kLoTileBytes, bar);
-            }
+            if (lane == 0 && r0 > 0) stage(t);   // round 0 was issued in the prologue
             mbar_wait(bar, phase);
             phase ^= 1;
             float* ts = tsum + w * kNC * kI;
