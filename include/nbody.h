@@ -84,9 +84,12 @@ typedef struct {
                              loopback != 0)                                    */
     int32_t world;        /* number of i-shards, 1 <= world <= n               */
     int32_t loopback;     /* != 0: emulate all `world` shards inside this one
-                             context on one GPU, shard by shard, with the
-                             exchange done in device memory (test mode; no
-                             NCCL).  Outputs then cover all n particles.       */
+                             context on one GPU, shard by shard (test mode; no
+                             NCCL).  Every shard packs into its own exchange
+                             buffer; the all-gather is emulated by one device
+                             copy per remote slice into it, issued between the
+                             same local-chunk and remote-chunk force launches
+                             an NCCL rank issues.  Outputs cover all n.        */
     int32_t jchunks;      /* max number of j-chunks of the canonical reduction
                              (0 -> 128).  Must be equal on every rank.          */
     int32_t hilo;         /* != 0: two-float positions (NEXT f2): packets also
@@ -98,7 +101,11 @@ typedef struct {
                              on rank 0, broadcast by the caller; required when
                              world > 1 and loopback == 0; optional with
                              world == 1 (then a 1-rank NCCL communicator is
-                             used for the exchange).                           */
+                             used for the exchange).  The communicator is
+                             non-blocking: every NCCL call waits at most
+                             NBODY_NCCL_TIMEOUT_S seconds (environment,
+                             default 600) to make progress, else NBODY_ENCCL
+                             (a missing or dead peer rank).                    */
     void* stream;         /* cudaStream_t to order work on; NULL -> the library
                              creates a non-blocking stream; pass
                              cudaStreamLegacy ((void*)1) for the legacy
@@ -137,8 +144,11 @@ int nbody_nccl_unique_id(uint8_t out[128]);
  * blocks until the copy is done, so the caller may free the inputs on
  * return.  Validation, returning NBODY_EINVAL with the
  * first bad index in the message: n >= 2; m finite and > 0; x and v finite;
- * G > 0; eps >= 0; dt > 0; 0 <= rank < world <= n; integrator known.
- * On error *out is NULL. */
+ * G > 0; eps >= 0; dt > 0; 0 <= rank < world <= n; integrator known; with
+ * eps > 0, G max(m) / eps^3 <= 1e30 (the fp32 range of the pair terms,
+ * G m_j / s^{3/2} <= G m_j / eps^3).  fp32(eps^2) below FLT_MIN (eps = 0, or
+ * subnormal, which the FTZ force pass flushes to 0) selects the guarded pass
+ * that excludes s == 0 (R#17).  On error *out is NULL. */
 int nbody_init(const nbody_config* cfg, const double* m, const double* x,
                const double* v, nbody_ctx** out);
 
@@ -253,11 +263,19 @@ int nbody_prof_launch_times(nbody_ctx* ctx, double* ms, int64_t cap, int64_t* co
 int nbody_prof_launch_sizes(nbody_ctx* ctx, int64_t* n_i, int64_t* n_j, int64_t cap,
                             int64_t* count);
 
+/* How steps were executed since init: shared-step CUDA-graph replays (one
+ * per step; block time steps: one per nbody_step call) and steps launched
+ * eagerly kernel by kernel (any output may be NULL).  Host-only. */
+int nbody_exec_stats(const nbody_ctx* ctx, int64_t* graph_launches, int64_t* eager_steps);
+
 /* Message for the last failure on ctx (or of the last failed nbody_init /
  * plan call when ctx is NULL).  Never NULL; valid until the next call. */
 const char* nbody_last_error(const nbody_ctx* ctx);
 
-/* Releases everything the context owns.  NULL is a no-op.  Collective. */
+/* Releases everything the context owns.  NULL is a no-op.  Collective for a
+ * healthy context (ncclCommFinalize, bounded by NBODY_NCCL_TIMEOUT_S); a
+ * context in the sticky failed state, or whose finalize times out, aborts its
+ * communicator (ncclCommAbort) and returns without waiting for peers. */
 void nbody_destroy(nbody_ctx* ctx);
 
 #ifdef __cplusplus

@@ -23,7 +23,7 @@ EXPORTS = (
     "nbody_compute_forces", "nbody_step", "nbody_energy", "nbody_get_state",
     "nbody_set_state", "nbody_sync", "nbody_prof_enable", "nbody_prof_read",
     "nbody_prof_launch_times", "nbody_prof_launch_sizes", "nbody_block_stats",
-    "nbody_get_derivs", "nbody_set_derivs", "nbody_set_levels",
+    "nbody_get_derivs", "nbody_set_derivs", "nbody_set_levels", "nbody_exec_stats",
     "nbody_last_error", "nbody_destroy",
 )
 
@@ -102,6 +102,7 @@ def lib():
         "nbody_get_derivs": ([p, p, p], ctypes.c_int),
         "nbody_set_derivs": ([p, p, p], ctypes.c_int),
         "nbody_set_levels": ([p, p], ctypes.c_int),
+        "nbody_exec_stats": ([p, P64, P64], ctypes.c_int),
         "nbody_last_error": ([p], ctypes.c_char_p),
         "nbody_destroy": ([p], None),
     }
@@ -160,6 +161,14 @@ class NBody:
     m: (n,), x, v: (3, n) float64 of the FULL system (torch CUDA/CPU tensors or
     numpy).  Work is ordered on ``stream`` (a torch.cuda.Stream, a raw
     cudaStream_t int, or None for torch's current stream).
+
+    Stream hygiene with a torch stream other than the current one: the library's
+    stream first waits on the current stream (inputs produced there are complete
+    before the library reads them); conversions and output tensors are made on the
+    library's stream, torch tensors the library writes are recorded on it (the
+    caching allocator will not hand their memory out while it is still in use), and
+    the current stream waits on the library's stream after every call that writes
+    tensors, so results are safe to consume in torch's current stream order.
     """
 
     def __init__(self, m, x, v, eps, dt, G=1.0, integrator="hermite", rank=0, world=1,
@@ -173,11 +182,14 @@ class NBody:
         if stream is None:
             stream = torch.cuda.current_stream(device)
         self.stream = stream
+        self._tstream = stream if hasattr(stream, "cuda_stream") else None   # torch stream object
         raw_stream = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
         if raw_stream == 0:
             raw_stream = 1   # cudaStreamLegacy: torch's default stream, not "library-created"
         self._keep = []
-        m, x, v = (self._prep(a) for a in (m, x, v))
+        self._enter()
+        with self._on_stream():
+            m, x, v = (self._prep(a) for a in (m, x, v))
         if m.ndim != 1:
             raise ValueError("m must be one-dimensional (n,)")
         n = int(m.shape[0])
@@ -209,6 +221,39 @@ class NBody:
         self.i0, self.i1 = i0.value, i1.value
         self.n_loc = self.i1 - self.i0
 
+    def _cur(self):
+        import torch
+        return torch.cuda.current_stream(self._tstream.device) if self._tstream is not None else None
+
+    def _enter(self):
+        """The library's stream waits on the current one (inputs made there are ready)."""
+        cur = self._cur()
+        if cur is not None and cur.cuda_stream != self._tstream.cuda_stream:
+            self._tstream.wait_stream(cur)
+
+    def _on_stream(self):
+        import contextlib
+        import torch
+        return torch.cuda.stream(self._tstream) if self._tstream is not None else contextlib.nullcontext()
+
+    def _written(self, *ts):
+        """Tensors the library wrote on its stream: keep their memory alive for it and
+        order the current stream after it."""
+        import torch
+        if self._tstream is None:
+            return
+        for t in ts:
+            if isinstance(t, torch.Tensor) and t.is_cuda:
+                t.record_stream(self._tstream)
+        cur = self._cur()
+        if cur.cuda_stream != self._tstream.cuda_stream:
+            cur.wait_stream(self._tstream)
+
+    def _empty3(self):
+        import torch
+        with self._on_stream():
+            return torch.empty((3, self.n_loc), dtype=torch.float64, device=self.device)
+
     @staticmethod
     def _prep(a):
         if isinstance(a, np.ndarray):
@@ -220,18 +265,18 @@ class NBody:
 
     def forces(self, acc=None, jerk=None):
         """(acc, jerk) of the local particles, (3, n_loc) float64 CUDA tensors."""
-        import torch
-        if acc is None:
-            acc = torch.empty((3, self.n_loc), dtype=torch.float64, device=self.device)
-        if jerk is None:
-            jerk = torch.empty((3, self.n_loc), dtype=torch.float64, device=self.device)
+        acc = self._empty3() if acc is None else acc
+        jerk = self._empty3() if jerk is None else jerk
         _want(acc, (3, self.n_loc), "acc")
         _want(jerk, (3, self.n_loc), "jerk")
+        self._enter()
         self._c(lib().nbody_compute_forces(self._ctx, _ptr(acc), _ptr(jerk)))
+        self._written(acc, jerk)
         return acc, jerk
 
     def step(self, nsteps=1):
         self._c(lib().nbody_step(self._ctx, int(nsteps)))
+        self._written()
 
     def energy(self):
         ke, pe = ctypes.c_double(), ctypes.c_double()
@@ -239,38 +284,38 @@ class NBody:
         return ke.value, pe.value
 
     def state(self, x=None, v=None):
-        import torch
-        if x is None:
-            x = torch.empty((3, self.n_loc), dtype=torch.float64, device=self.device)
-        if v is None:
-            v = torch.empty((3, self.n_loc), dtype=torch.float64, device=self.device)
+        x = self._empty3() if x is None else x
+        v = self._empty3() if v is None else v
         _want(x, (3, self.n_loc), "x")
         _want(v, (3, self.n_loc), "v")
+        self._enter()
         self._c(lib().nbody_get_state(self._ctx, _ptr(x), _ptr(v)))
+        self._written(x, v)
         return x, v
 
     def set_state(self, x, v, keep_forces=False):
         """Overwrite the local (3, n_loc) positions and/or velocities (None keeps them)."""
         _want(x, (3, self.n_loc), "x")
         _want(v, (3, self.n_loc), "v")
+        self._enter()
         self._c(lib().nbody_set_state(self._ctx, _ptr(x), _ptr(v), 1 if keep_forces else 0))
 
     def derivs(self, acc=None, jerk=None):
         """(acc, jerk) the next step starts from, (3, n_loc) float64 (checkpointing)."""
-        import torch
-        if acc is None:
-            acc = torch.empty((3, self.n_loc), dtype=torch.float64, device=self.device)
-        if jerk is None:
-            jerk = torch.empty((3, self.n_loc), dtype=torch.float64, device=self.device)
+        acc = self._empty3() if acc is None else acc
+        jerk = self._empty3() if jerk is None else jerk
         _want(acc, (3, self.n_loc), "acc")
         _want(jerk, (3, self.n_loc), "jerk")
+        self._enter()
         self._c(lib().nbody_get_derivs(self._ctx, _ptr(acc), _ptr(jerk)))
+        self._written(acc, jerk)
         return acc, jerk
 
     def set_derivs(self, acc, jerk=None):
         """Restore saved derivatives (exact resume; jerk unused by leapfrog)."""
         _want(acc, (3, self.n_loc), "acc")
         _want(jerk, (3, self.n_loc), "jerk")
+        self._enter()
         self._c(lib().nbody_set_derivs(self._ctx, _ptr(acc), _ptr(jerk)))
 
     def set_levels(self, level):
@@ -316,6 +361,12 @@ class NBody:
         self._c(lib().nbody_block_stats(self._ctx, ctypes.byref(bs), ctypes.byref(asum),
                                         None if lev is None else lev.ctypes.data))
         return (bs.value, asum.value, lev) if levels else (bs.value, asum.value)
+
+    def exec_stats(self):
+        """(CUDA-graph launches, eagerly launched steps) since init."""
+        g, e = ctypes.c_int64(), ctypes.c_int64()
+        self._c(lib().nbody_exec_stats(self._ctx, ctypes.byref(g), ctypes.byref(e)))
+        return g.value, e.value
 
     def close(self):
         if getattr(self, "_ctx", None):

@@ -52,14 +52,9 @@ namespace {
 #ifndef FK_MINB
 #define FK_MINB 2
 #endif
-#ifndef FK_RCP
-#define FK_RCP 0
-#endif
-#ifndef FK_HYB
-#define FK_HYB 0         // fp64 i-particles per thread on the FP64 pipe (measured slower; 0: off)
-#endif
-#ifndef FK_HYB_NEWTON
-#define FK_HYB_NEWTON 1  // Newton step after rsqrt.approx.f64
+#ifndef FK_PIPE
+#define FK_PIPE 0        // software-pipelined j loop: rsqrt of j + 1 issued before j's sums
+                         // (2: the same, hand-unrolled by two with ping-pong operands)
 #endif
 #ifndef FK_MINB_ACC
 #define FK_MINB_ACC 2    // acceleration-only kernel (leapfrog)
@@ -91,25 +86,24 @@ constexpr int kLoTileBytes = kTile * (int)sizeof(float4);   // hi/lo position ta
 static_assert(kStages * 8 <= 64, "mbarrier area");
 
 // CTA shape: P packed i-pairs per thread, T threads, MINB resident CTAs per SM
-// (launch bounds), HYB fp64 i per thread.  Two shapes are instantiated: the
+// (launch bounds).  Two shapes are instantiated: the
 // default (1024 i per CTA) and a small one (256 i per CTA) for launches with
 // few i -- block-step active sets and small N -- where 1024-i CTAs would leave
 // most SMs idle.  Every i's j loop is identical in both, so results are too.
-template <int P, int T, int MINB, int MINB_ACC, int HYB, int U = FK_UNROLL, int UL = U>
+template <int P, int T, int MINB, int MINB_ACC, int U = FK_UNROLL, int UL = U, int PIPE = FK_PIPE>
 struct FkCfg {
-    static constexpr int kPairs = P, kThreads = T, kMinB = MINB, kMinBAcc = MINB_ACC, kHyb = HYB;
+    static constexpr int kPairs = P, kThreads = T, kMinB = MINB, kMinBAcc = MINB_ACC;
+    static constexpr int kPipe = PIPE;    // software-pipelined j loop (0: off)
     static constexpr int kUnrollJ = U, kUnrollList = UL;   // j-loop unroll: plain / active-list
-    static constexpr int kIPerBlock = (2 * P + HYB) * T;
-    static constexpr int kT64TileBytes = HYB ? kTile * (int)sizeof(JPkt64) : 0;   // fp64 j tiles
+    static constexpr int kIPerBlock = 2 * P * T;
     static constexpr int kAccSmemBytes = FK_ACC_SMEM ? 6 * 2 * P * T * 8 : 0;
-    // shared memory: [ring: kStages j-tiles][ring_lo: kStages lo-tiles][fp64 tiles][64 B mbarriers][fp64 acc]
+    // shared memory: [ring: kStages j-tiles][ring_lo: kStages lo-tiles][64 B mbarriers][fp64 acc]
     static constexpr int kOffLo = kStages * kTileBytes;
-    static constexpr int kOff64 = kOffLo + kStages * kLoTileBytes;
-    static constexpr int kOffBar = kOff64 + kStages * kT64TileBytes;
+    static constexpr int kOffBar = kOffLo + kStages * kLoTileBytes;
     static constexpr int kOffAcc = kOffBar + 64;
     static constexpr int kSmemBytes = kOffAcc + kAccSmemBytes;
 };
-using CfgBig = FkCfg<FK_PAIRS, FK_THREADS, FK_MINB, FK_MINB_ACC, FK_HYB>;
+using CfgBig = FkCfg<FK_PAIRS, FK_THREADS, FK_MINB, FK_MINB_ACC>;
 #ifndef FK_SMALL_PAIRS
 #define FK_SMALL_PAIRS 1
 #endif
@@ -119,10 +113,9 @@ using CfgBig = FkCfg<FK_PAIRS, FK_THREADS, FK_MINB, FK_MINB_ACC, FK_HYB>;
 #ifndef FK_SMALL_MINB
 #define FK_SMALL_MINB 6
 #endif
-using CfgSmall = FkCfg<FK_SMALL_PAIRS, FK_SMALL_THREADS, FK_SMALL_MINB, FK_SMALL_MINB, 0, FK_SMALL_UNROLL,
+using CfgSmall = FkCfg<FK_SMALL_PAIRS, FK_SMALL_THREADS, FK_SMALL_MINB, FK_SMALL_MINB, FK_SMALL_UNROLL,
                        FK_SMALL_LIST_UNROLL>;
 constexpr int kIPerBlock = CfgBig::kIPerBlock;
-constexpr int kHyb = CfgBig::kHyb;
 
 typedef unsigned long long f2;  // packed {lo, hi} fp32 pair in one 64-bit register
 
@@ -149,16 +142,6 @@ __device__ __forceinline__ f2 ffma2(f2 a, f2 b, f2 c) {
     f2 d;
     asm("fma.rn.ftz.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
     return d;
-}
-__device__ __forceinline__ double rsqrt_approx_f64(double s) {
-    double r;
-    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(s));   // MUFU.RSQ64H, no slow path
-    return r;
-}
-[[maybe_unused]] __device__ __forceinline__ float rcp_ftz(float s) {
-    float r;
-    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(s));
-    return r;
 }
 __device__ __forceinline__ float rsqrt_ftz(float s) {
     float r;
@@ -242,6 +225,35 @@ __device__ __forceinline__ JOps load_jops(const JPkt* tile, const float4* tile_l
     return jo;
 }
 
+struct JOps1 {
+    float x, y, z, m, eps2, vx, vy, vz, lx, ly, lz;
+};
+struct IOne {
+    float nx, ny, nz, nvx, nvy, nvz, nlx, nly, nlz;
+};
+template <bool kJerk, bool kHiLo>
+__device__ __forceinline__ JOps1 load_jops1(const JPkt* tile, const float4* tile_lo, int jj) {
+    const float4 P = jpkt_pos(tile[jj]), V = jpkt_vel(tile[jj]);
+    JOps1 j{P.x, P.y, P.z, P.w, V.w, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    if (kJerk) { j.vx = V.x; j.vy = V.y; j.vz = V.z; }
+    if (kHiLo) {
+        const float4 L = tile_lo[jj];
+        j.lx = L.x; j.ly = L.y; j.lz = L.z;
+    }
+    return j;
+}
+
+// the packed operands of a scalar j (the pipelined loops carry j as scalars across
+// iterations and broadcast at the use, so no {v, v} register pairs are materialised)
+__device__ __forceinline__ JOps bcast(const JOps1& s) {
+    JOps j;
+    j.x = f2bc(s.x); j.y = f2bc(s.y); j.z = f2bc(s.z); j.m = f2bc(s.m); j.eps2 = f2bc(s.eps2);
+    j.vx = f2bc(s.vx); j.vy = f2bc(s.vy); j.vz = f2bc(s.vz);
+    j.lx = f2bc(s.lx); j.ly = f2bc(s.ly); j.lz = f2bc(s.lz);
+    j.mass = s.m;
+    return j;
+}
+
 // negated i state of the particle in packet src (0 for a padding slot)
 template <bool kHiLo>
 __device__ __forceinline__ void load_i(const ForceArgs& a, bool valid, int64_t src, float (&q)[9]) {
@@ -277,26 +289,33 @@ __device__ __forceinline__ void report_coincident(const GuardCtx& g, int sl, int
     if (ig != jg) atomicMin(g.coincident, (unsigned long long)ig);
 }
 
-// One j against one packed i-pair: the FP32 interaction of the file header,
-// accumulated into pair p's tile sums acc[0..kNC)[p]; m3 = {-3, -3}.  Every force kernel
-// (all CTA shapes, the tile-split active-list kernel) runs exactly this
-// instruction sequence per lane, so their tile sums are bit-identical.
-// kGuard (eps = 0): s == 0 gives ri = 0 and reports a coincident pair of
-// distinct particles; sl_lo / sl_hi are the lanes' i-slots.
-template <bool kGuard, bool kJerk, bool kHiLo, bool kList, int kNC, int kP>
-__device__ __forceinline__ void interact(const JOps& j, const IPair& i, f2 (&acc)[kNC][kP], int p,
-                                         f2 m3, int sl_lo, int sl_hi, int64_t jg, const GuardCtx& g) {
-    f2 dx = fadd2(j.x, i.nx);
-    f2 dy = fadd2(j.y, i.ny);
-    f2 dz = fadd2(j.z, i.nz);
+// One j against one packed i-pair: the FP32 interaction of the file header, in two
+// halves.  front(): d = x_j - x_i (hi/lo: + the tails), s = |d|^2 + eps^2, ri = 1/sqrt(s)
+// (MUFU.RSQ); back(): mr3 = G m_j ri^3, a += mr3 d, jerk += mr3 (w - 3 (d.w) ri^2 d).
+// interact() runs both; the software-pipelined j loop of force_kernel runs front() of
+// j + 1 before back() of j, so each MUFU.RSQ has a whole j step of independent work to
+// hide behind.  Every force kernel (all CTA shapes, pipelined or not, the tile-split
+// kernels) runs exactly this instruction sequence per lane, so their tile sums are
+// bit-identical.  m3 = {-3, -3}.  kGuard (eps = 0): s == 0 gives ri = 0 and reports a
+// coincident pair of distinct particles; sl_lo / sl_hi are the lanes' i-slots.
+struct Front {
+    f2 dx, dy, dz, ri;
+};
+template <bool kGuard, bool kHiLo, bool kList>
+__device__ __forceinline__ Front front(const JOps& j, const IPair& i, int sl_lo, int sl_hi, int64_t jg,
+                                       const GuardCtx& g) {
+    Front f;
+    f.dx = fadd2(j.x, i.nx);
+    f.dy = fadd2(j.y, i.ny);
+    f.dz = fadd2(j.z, i.nz);
     if (kHiLo) {   // d = (x_j^hi - x_i^hi) + (x_j^lo - x_i^lo)   (NEXT f2)
-        dx = fadd2(dx, fadd2(j.lx, i.nlx));
-        dy = fadd2(dy, fadd2(j.ly, i.nly));
-        dz = fadd2(dz, fadd2(j.lz, i.nlz));
+        f.dx = fadd2(f.dx, fadd2(j.lx, i.nlx));
+        f.dy = fadd2(f.dy, fadd2(j.ly, i.nly));
+        f.dz = fadd2(f.dz, fadd2(j.lz, i.nlz));
     }
-    f2 s2 = ffma2(dx, dx, j.eps2);
-    s2 = ffma2(dy, dy, s2);
-    s2 = ffma2(dz, dz, s2);
+    f2 s2 = ffma2(f.dx, f.dx, j.eps2);
+    s2 = ffma2(f.dy, f.dy, s2);
+    s2 = ffma2(f.dz, f.dz, s2);
     float s_lo, s_hi;
     f2split(s2, s_lo, s_hi);
     float r_lo = rsqrt_ftz(s_lo), r_hi = rsqrt_ftz(s_hi);
@@ -310,42 +329,47 @@ __device__ __forceinline__ void interact(const JOps& j, const IPair& i, f2 (&acc
             report_coincident<kList>(g, sl_hi, jg, j.mass);
         }
     }
-    const f2 ri = f2make(r_lo, r_hi);
-#if FK_RCP   // 1/s from MUFU.RCP (XU pipe) instead of ri * ri on the FMA pipe
-    f2 ri2 = f2make(rcp_ftz(s_lo), rcp_ftz(s_hi));
-    if (kGuard) ri2 = fmul2(ri, ri);
-#else
-    const f2 ri2 = fmul2(ri, ri);
-#endif
-    const f2 mr3 = fmul2(fmul2(j.m, ri), ri2);      // G m_j / s^{3/2}
-    acc[0][p] = ffma2(mr3, dx, acc[0][p]);
-    acc[1][p] = ffma2(mr3, dy, acc[1][p]);
-    acc[2][p] = ffma2(mr3, dz, acc[2][p]);
+    f.ri = f2make(r_lo, r_hi);
+    return f;
+}
+template <bool kJerk, int kNC, int kP>
+__device__ __forceinline__ void back(const JOps& j, const IPair& i, const Front& f, f2 (&acc)[kNC][kP], int p,
+                                     f2 m3) {
+    const f2 ri2 = fmul2(f.ri, f.ri);
+    const f2 mr3 = fmul2(fmul2(j.m, f.ri), ri2);   // G m_j / s^{3/2}
+    acc[0][p] = ffma2(mr3, f.dx, acc[0][p]);
+    acc[1][p] = ffma2(mr3, f.dy, acc[1][p]);
+    acc[2][p] = ffma2(mr3, f.dz, acc[2][p]);
     if (kJerk) {
         const f2 wx = fadd2(j.vx, i.nvx);
         const f2 wy = fadd2(j.vy, i.nvy);
         const f2 wz = fadd2(j.vz, i.nvz);
-        f2 rv = fmul2(dx, wx);
-        rv = ffma2(dy, wy, rv);
-        rv = ffma2(dz, wz, rv);                     // d . w
+        f2 rv = fmul2(f.dx, wx);
+        rv = ffma2(f.dy, wy, rv);
+        rv = ffma2(f.dz, wz, rv);                   // d . w
         const f2 q3 = fmul2(fmul2(rv, ri2), m3);    // -3 (d.w) / s
-        acc[3 % kNC][p] = ffma2(mr3, ffma2(q3, dx, wx), acc[3 % kNC][p]);
-        acc[4 % kNC][p] = ffma2(mr3, ffma2(q3, dy, wy), acc[4 % kNC][p]);
-        acc[5 % kNC][p] = ffma2(mr3, ffma2(q3, dz, wz), acc[5 % kNC][p]);
+        acc[3 % kNC][p] = ffma2(mr3, ffma2(q3, f.dx, wx), acc[3 % kNC][p]);
+        acc[4 % kNC][p] = ffma2(mr3, ffma2(q3, f.dy, wy), acc[4 % kNC][p]);
+        acc[5 % kNC][p] = ffma2(mr3, ffma2(q3, f.dz, wz), acc[5 % kNC][p]);
     }
+}
+template <bool kGuard, bool kJerk, bool kHiLo, bool kList, int kNC, int kP>
+__device__ __forceinline__ void interact(const JOps& j, const IPair& i, f2 (&acc)[kNC][kP], int p,
+                                         f2 m3, int sl_lo, int sl_hi, int64_t jg, const GuardCtx& g) {
+    const Front f = front<kGuard, kHiLo, kList>(j, i, sl_lo, sl_hi, jg, g);
+    back<kJerk>(j, i, f, acc, p, m3);
 }
 
 template <bool kGuard, bool kJerk, bool kHiLo, class C, bool kList = false>
 __global__ void __launch_bounds__(C::kThreads, kJerk ? C::kMinB : C::kMinBAcc) force_kernel(ForceArgs a) {
-    constexpr int kPairs = C::kPairs, kThreads = C::kThreads, kHyb = C::kHyb;
-    constexpr int kIPerBlock = C::kIPerBlock, kT64TileBytes = C::kT64TileBytes;
-    constexpr int kOffLo = C::kOffLo, kOff64 = C::kOff64, kOffBar = C::kOffBar, kOffAcc = C::kOffAcc;
+    constexpr int kPairs = C::kPairs, kThreads = C::kThreads;
+    constexpr int kIPerBlock = C::kIPerBlock;
+    constexpr int kOffLo = C::kOffLo, kOffBar = C::kOffBar, kOffAcc = C::kOffAcc;
     constexpr int kNC = kJerk ? 6 : 3;   // accumulated components: a (+ jerk)
-    constexpr uint32_t kStageTx = kTileBytes + (kHiLo ? kLoTileBytes : 0) + kT64TileBytes;
+    constexpr uint32_t kStageTx = kTileBytes + (kHiLo ? kLoTileBytes : 0);
     extern __shared__ __align__(128) unsigned char smem[];
     JPkt* ring = reinterpret_cast<JPkt*>(smem);
     float4* ring_lo = reinterpret_cast<float4*>(smem + kOffLo);
-    JPkt64* ring64 = reinterpret_cast<JPkt64*>(smem + kOff64);
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + kOffBar);
 
     const int tid = threadIdx.x;
@@ -412,25 +436,6 @@ __global__ void __launch_bounds__(C::kThreads, kJerk ? C::kMinB : C::kMinBAcc) f
         }
     }
 
-    // ---- fp64 i-particles (slots 2*kPairs .. 2*kPairs+kHyb-1 of the thread): exact fp64
-    //      state, interactions on the FP64 pipe, accumulated in fp64 over the chunk
-    double hx[kHyb > 0 ? kHyb : 1], hy[kHyb > 0 ? kHyb : 1], hz[kHyb > 0 ? kHyb : 1];
-    double hvx[kHyb > 0 ? kHyb : 1], hvy[kHyb > 0 ? kHyb : 1], hvz[kHyb > 0 ? kHyb : 1];
-    double hacc[kNC][kHyb > 0 ? kHyb : 1];
-#pragma unroll
-    for (int h = 0; h < kHyb; ++h) {
-        const int il = ib + (2 * kPairs + h) * kThreads + tid;
-        if (il < n_loc) {
-            const JPkt64 pk = a.pk64[a.i_base + (kList ? a.ilist[il] : il)];
-            hx[h] = pk.p.x; hy[h] = pk.p.y; hz[h] = pk.p.z;
-            hvx[h] = pk.v.x; hvy[h] = pk.v.y; hvz[h] = pk.v.z;
-        } else {
-            hx[h] = hy[h] = hz[h] = hvx[h] = hvy[h] = hvz[h] = 0.0;
-        }
-#pragma unroll
-        for (int k = 0; k < kNC; ++k) hacc[k][h] = 0.0;
-    }
-
 #if FK_ACC_SMEM
     // fp64 chunk accumulators in shared memory: [k][l][tid], conflict-free
     double* acc_s = reinterpret_cast<double*>(smem + kOffAcc);
@@ -451,9 +456,6 @@ __global__ void __launch_bounds__(C::kThreads, kJerk ? C::kMinB : C::kMinBAcc) f
             if (kHiLo)
                 tma_load_1d(ring_lo + s * kTile, a.pklo + jc0 + (int64_t)s * kTile, kLoTileBytes,
                             &full[s]);
-            if (kHyb)
-                tma_load_1d(ring64 + s * kTile, a.pk64 + jc0 + (int64_t)s * kTile, kT64TileBytes,
-                            &full[s]);
         }
     }
 
@@ -469,7 +471,6 @@ __global__ void __launch_bounds__(C::kThreads, kJerk ? C::kMinB : C::kMinBAcc) f
         mbar_wait(&full[s], (uint32_t)((t / kStages) & 1));
         const JPkt* tile = ring + s * kTile;
         const float4* tile_lo = ring_lo + s * kTile;
-        const JPkt64* tile64 = ring64 + s * kTile;
 
         f2 acc[kNC][kPairs];
 #pragma unroll
@@ -477,52 +478,75 @@ __global__ void __launch_bounds__(C::kThreads, kJerk ? C::kMinB : C::kMinBAcc) f
 #pragma unroll
             for (int p = 0; p < kPairs; ++p) acc[k][p] = 0ull;
 
-#pragma unroll(kList ? C::kUnrollList : C::kUnrollJ)
-        for (int jj = 0; jj < kTile; ++jj) {
-            const JOps jo = load_jops<kJerk, kHiLo>(tile, tile_lo, jj);
-            const int64_t jg = kGuard ? jc0 + (int64_t)t * kTile + jj : 0;
+        const int64_t jt0 = jc0 + (int64_t)t * kTile;   // global index of the tile's first j
+        if constexpr (C::kPipe == 2) {
+            // the pipeline hand-unrolled by two: operands alternate between (ja, fa) and
+            // (jb, fb), so no register copies are needed at the loop back edge
+            auto fronts = [&](const JOps1& j1, Front (&f)[kPairs], int jj) {
+                const JOps jo = bcast(j1);
+#pragma unroll
+                for (int p = 0; p < kPairs; ++p)
+                    f[p] = front<kGuard, kHiLo, kList>(jo, ip[p], ib + 2 * p * kThreads + tid,
+                                                       ib + (2 * p + 1) * kThreads + tid,
+                                                       kGuard ? jt0 + jj : 0, gc);
+            };
+            auto backs = [&](const JOps1& j1, const Front (&f)[kPairs]) {
+                const JOps jo = bcast(j1);
+#pragma unroll
+                for (int p = 0; p < kPairs; ++p) back<kJerk>(jo, ip[p], f[p], acc, p, m3);
+            };
+            static_assert(kTile % 2 == 0, "ping-pong pipeline");
+            JOps1 ja = load_jops1<kJerk, kHiLo>(tile, tile_lo, 0), jb;
+            Front fa[kPairs], fb[kPairs];
+            fronts(ja, fa, 0);
+#pragma unroll 1
+            for (int jj = 0; jj < kTile - 2; jj += 2) {
+                jb = load_jops1<kJerk, kHiLo>(tile, tile_lo, jj + 1);
+                fronts(jb, fb, jj + 1);
+                backs(ja, fa);
+                ja = load_jops1<kJerk, kHiLo>(tile, tile_lo, jj + 2);
+                fronts(ja, fa, jj + 2);
+                backs(jb, fb);
+            }
+            jb = load_jops1<kJerk, kHiLo>(tile, tile_lo, kTile - 1);
+            fronts(jb, fb, kTile - 1);
+            backs(ja, fa);
+            backs(jb, fb);
+        } else if constexpr (C::kPipe == 1) {
+            // software pipeline: front() of j + 1 (its MUFU.RSQ) is issued in the same loop
+            // body as back() of j, whose operands arrived one iteration earlier
+            JOps1 jc = load_jops1<kJerk, kHiLo>(tile, tile_lo, 0);
+            Front fr[kPairs];
 #pragma unroll
             for (int p = 0; p < kPairs; ++p)
-                interact<kGuard, kJerk, kHiLo, kList>(jo, ip[p], acc, p, m3, ib + 2 * p * kThreads + tid,
-                                                      ib + (2 * p + 1) * kThreads + tid, jg, gc);
-            // ---- the same interaction in fp64 for the thread's kHyb fp64 i-particles.
-            //      DADD/DFMA/DMUL issue to the FP64 pipe, which runs beside FFMA2
-            //      (scripts/ubench_fp32.cu: 4 FFMA2 : 3 DFMA keeps ~95 % of the FP32 rate).
-            if (kHyb) {
-                const double4 Pd = tile64[jj].p;   // x, y, z, G m
-                const double4 Vd = tile64[jj].v;   // vx, vy, vz, eps2
+                fr[p] = front<kGuard, kHiLo, kList>(bcast(jc), ip[p], ib + 2 * p * kThreads + tid,
+                                                    ib + (2 * p + 1) * kThreads + tid, kGuard ? jt0 : 0, gc);
+#pragma unroll(kList ? C::kUnrollList : C::kUnrollJ)
+            for (int jj = 0; jj < kTile - 1; ++jj) {
+                const JOps1 jn = load_jops1<kJerk, kHiLo>(tile, tile_lo, jj + 1);
+                Front fn[kPairs];
 #pragma unroll
-                for (int h = 0; h < kHyb; ++h) {
-                    const double dx = Pd.x - hx[h], dy = Pd.y - hy[h], dz = Pd.z - hz[h];
-                    const double s = fma(dz, dz, fma(dy, dy, fma(dx, dx, Vd.w)));
-                    double ri = rsqrt_approx_f64(s);
-#if FK_HYB_NEWTON
-                    ri = ri * fma(-0.5 * s, ri * ri, 1.5);
-#endif
-                    if (kGuard) {
-                        if (s == 0.0) {
-                            ri = 0.0;
-                            const int sl = ib + (2 * kPairs + h) * kThreads + tid;
-                            const int64_t ig = a.i_base + (kList && sl < n_loc ? a.ilist[sl] : sl);
-                            const int64_t jg = jc0 + (int64_t)t * kTile + jj;
-                            if (ig != jg && sl < n_loc && Pd.w != 0.0)
-                                atomicMin(a.coincident, (unsigned long long)ig);
-                        }
-                    }
-                    const double ri2 = ri * ri;
-                    const double mr3 = Pd.w * ri * ri2;
-                    hacc[0][h] = fma(mr3, dx, hacc[0][h]);
-                    hacc[1][h] = fma(mr3, dy, hacc[1][h]);
-                    hacc[2][h] = fma(mr3, dz, hacc[2][h]);
-                    if (kJerk) {
-                        const double wx = Vd.x - hvx[h], wy = Vd.y - hvy[h], wz = Vd.z - hvz[h];
-                        const double rv = fma(dz, wz, fma(dy, wy, dx * wx));
-                        const double q3 = -3.0 * rv * ri2;
-                        hacc[3 % kNC][h] = fma(mr3, fma(q3, dx, wx), hacc[3 % kNC][h]);
-                        hacc[4 % kNC][h] = fma(mr3, fma(q3, dy, wy), hacc[4 % kNC][h]);
-                        hacc[5 % kNC][h] = fma(mr3, fma(q3, dz, wz), hacc[5 % kNC][h]);
-                    }
-                }
+                for (int p = 0; p < kPairs; ++p)
+                    fn[p] = front<kGuard, kHiLo, kList>(bcast(jn), ip[p], ib + 2 * p * kThreads + tid,
+                                                        ib + (2 * p + 1) * kThreads + tid,
+                                                        kGuard ? jt0 + jj + 1 : 0, gc);
+#pragma unroll
+                for (int p = 0; p < kPairs; ++p) back<kJerk>(bcast(jc), ip[p], fr[p], acc, p, m3);
+                jc = jn;
+#pragma unroll
+                for (int p = 0; p < kPairs; ++p) fr[p] = fn[p];
+            }
+#pragma unroll
+            for (int p = 0; p < kPairs; ++p) back<kJerk>(bcast(jc), ip[p], fr[p], acc, p, m3);
+        } else {
+#pragma unroll(kList ? C::kUnrollList : C::kUnrollJ)
+            for (int jj = 0; jj < kTile; ++jj) {
+                const JOps jo = load_jops<kJerk, kHiLo>(tile, tile_lo, jj);
+                const int64_t jg = kGuard ? jt0 + jj : 0;
+#pragma unroll
+                for (int p = 0; p < kPairs; ++p)
+                    interact<kGuard, kJerk, kHiLo, kList>(jo, ip[p], acc, p, m3, ib + 2 * p * kThreads + tid,
+                                                          ib + (2 * p + 1) * kThreads + tid, jg, gc);
             }
         }
         // tile sum -> fp64, ascending tile order
@@ -543,9 +567,6 @@ __global__ void __launch_bounds__(C::kThreads, kJerk ? C::kMinB : C::kMinBAcc) f
             if (kHiLo)
                 tma_load_1d(ring_lo + s * kTile, a.pklo + jc0 + (int64_t)(t + kStages) * kTile,
                             kLoTileBytes, &full[s]);
-            if (kHyb)
-                tma_load_1d(ring64 + s * kTile, a.pk64 + jc0 + (int64_t)(t + kStages) * kTile,
-                            kT64TileBytes, &full[s]);
         }
     }
 
@@ -559,14 +580,6 @@ __global__ void __launch_bounds__(C::kThreads, kJerk ? C::kMinB : C::kMinBAcc) f
         if (il < n_loc) {
 #pragma unroll
             for (int k = 0; k < kNC; ++k) out[(int64_t)k * a.n_loc_pad + il] = ACC64(k, l);
-        }
-    }
-#pragma unroll
-    for (int h = 0; h < kHyb; ++h) {
-        const int il = ib + (2 * kPairs + h) * kThreads + tid;
-        if (il < n_loc) {
-#pragma unroll
-            for (int k = 0; k < kNC; ++k) out[(int64_t)k * a.n_loc_pad + il] = hacc[k][h];
         }
     }
 #undef ACC64
@@ -621,24 +634,6 @@ __device__ __forceinline__ float ffma1(float a, float b, float c) {
     return d;
 }
 
-struct JOps1 {
-    float x, y, z, m, eps2, vx, vy, vz, lx, ly, lz;
-};
-struct IOne {
-    float nx, ny, nz, nvx, nvy, nvz, nlx, nly, nlz;
-};
-template <bool kJerk, bool kHiLo>
-__device__ __forceinline__ JOps1 load_jops1(const JPkt* tile, const float4* tile_lo, int jj) {
-    const float4 P = jpkt_pos(tile[jj]), V = jpkt_vel(tile[jj]);
-    JOps1 j{P.x, P.y, P.z, P.w, V.w, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-    if (kJerk) { j.vx = V.x; j.vy = V.y; j.vz = V.z; }
-    if (kHiLo) {
-        const float4 L = tile_lo[jj];
-        j.lx = L.x; j.ly = L.y; j.lz = L.z;
-    }
-    return j;
-}
-
 // interact() on one lane: the same operations in the same order (FTZ, RN), so
 // each lane's tile sum equals the corresponding lane of the packed form
 template <bool kGuard, bool kJerk, bool kHiLo, bool kList, int kNC>
@@ -660,12 +655,7 @@ __device__ __forceinline__ void interact1(const JOps1& j, const IOne& i, float (
         ri = 0.f;
         report_coincident<kList>(g, sl, jg, j.m);
     }
-#if FK_RCP
-    float ri2 = rcp_ftz(s2);
-    if (kGuard) ri2 = fmul1(ri, ri);
-#else
     const float ri2 = fmul1(ri, ri);
-#endif
     const float mr3 = fmul1(fmul1(j.m, ri), ri2);
     acc[0] = ffma1(mr3, dx, acc[0]);
     acc[1] = ffma1(mr3, dy, acc[1]);
@@ -807,7 +797,6 @@ int force_i_per_block() { return kIPerBlock; }
 int force_tsplit_i_per_block(bool scalar) { return scalar ? 32 : 64; }
 int force_tsplit_threads(int chunk) { return 32 * std::max(1, std::min(kTsWarpsMax, chunk / kTile)); }
 int force_list_i_per_block(bool big) { return big ? CfgBig::kIPerBlock : CfgSmall::kIPerBlock; }
-int force_hyb() { return kHyb; }
 
 int sm_count();
 
@@ -926,7 +915,6 @@ int sm_count() {
 // the GPU (its per-CTA efficiency is within ~10 % of the default's,
 // profiles/r01_sweep_force.txt p1b6, and it quarters the idle i-slots).
 bool use_small_cta(const ForceArgs& a) {
-    if (kHyb != 0) return false;
     const char* ov = getenv("NBODY_FORCE_CTA");   // tests: small | big (default: by size)
     if (ov && !strcmp(ov, "small")) return true;
     if (ov && (!strcmp(ov, "big") || !strcmp(ov, "tiny"))) return false;
@@ -937,7 +925,6 @@ bool use_small_cta(const ForceArgs& a) {
 // Launches whose 256-i CTAs would not give every SM one CTA (N ~ 1 000) are
 // latency-bound: the scalar tile-split kernel runs them with 32 i per warp.
 bool use_tiny(const ForceArgs& a) {
-    if (kHyb != 0) return false;
     const char* ov = getenv("NBODY_FORCE_CTA");
     if (ov && *ov) return !strcmp(ov, "tiny");
     const int64_t ctas = (int64_t)((a.n_loc + CfgSmall::kIPerBlock - 1) / CfgSmall::kIPerBlock) * a.c_count;
@@ -948,6 +935,12 @@ cudaError_t launch_force_list(const ForceArgs& a, bool guard_self, bool big, cud
     if (a.c_count <= 0 || a.n_loc <= 0) return cudaSuccess;
     if (!a.ilist) return cudaErrorInvalidValue;
     return big ? launch_cfg<CfgBig>(a, guard_self, true, s) : launch_cfg<CfgSmall>(a, guard_self, true, s);
+}
+
+cudaError_t launch_force_big(const ForceArgs& a, bool guard_self, bool jerk, cudaStream_t s) {
+    if (a.c_count <= 0 || a.n_loc <= 0) return cudaSuccess;
+    if (a.ilist) return cudaErrorInvalidValue;
+    return launch_cfg<CfgBig>(a, guard_self, jerk, s);
 }
 
 cudaError_t launch_force(const ForceArgs& a, bool guard_self, bool jerk, cudaStream_t s) {

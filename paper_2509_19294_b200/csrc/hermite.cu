@@ -48,12 +48,6 @@ __device__ __forceinline__ void store_packet(const StateArgs& a, int64_t k, cons
     const float qx = __double2float_rn(v[0]), qy = __double2float_rn(v[1]);
     const float qz = __double2float_rn(v[2]);
     a.pkt[k] = make_jpkt(px, py, pz, pm, qx, qy, qz, a.eps2);
-    if (a.pk64) {   // exact fp64 copy for the force kernel's FP64-pipe i-particles
-        JPkt64 q;
-        q.p = make_double4(x[0], x[1], x[2], gm);
-        q.v = make_double4(v[0], v[1], v[2], (double)a.eps2);
-        a.pk64[k] = q;
-    }
     if (a.pklo)
         a.pklo[k] = make_float4(__double2float_rn(x[0] - (double)px),
                                 __double2float_rn(x[1] - (double)py),
@@ -191,19 +185,12 @@ __global__ void correct_predict_pack_kernel(StateArgs a) {
     }
 }
 
-__global__ void fill_padding_kernel(JPkt* pkt, float4* pklo, JPkt64* pk64, int64_t from, int64_t to,
-                                    float eps2) {
+__global__ void fill_padding_kernel(JPkt* pkt, float4* pklo, int64_t from, int64_t to, float eps2) {
     for (int64_t k = from + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < to;
          k += (int64_t)gridDim.x * blockDim.x) {
         // zero mass far away: contributes exactly 0 (padding)
         pkt[k] = make_jpkt(1e18f, 1e18f, 1e18f, 0.f, 0.f, 0.f, 0.f, eps2);
         if (pklo) pklo[k] = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (pk64) {
-            JPkt64 q;
-            q.p = make_double4(1e18, 1e18, 1e18, 0.0);
-            q.v = make_double4(0.0, 0.0, 0.0, (double)eps2);
-            pk64[k] = q;
-        }
     }
 }
 
@@ -211,6 +198,7 @@ __global__ void validate_kernel(StateArgs a, unsigned long long* bad2) {
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < a.n_loc; i += gridDim.x * blockDim.x) {
         const double mi = a.m[i];
         if (!(isfinite(mi) && mi > 0.0)) flag_bad(&bad2[0], a.i_base + i);
+        else atomicMax(&bad2[2], (unsigned long long)__double_as_longlong(mi));   // max mass (> 0: bits order)
         bool ok = true;
         for (int c = 0; c < 3; ++c)
             ok = ok && isfinite(a.x[c * a.n_loc_pad + i]) && isfinite(a.v[c * a.n_loc_pad + i]);
@@ -634,10 +622,9 @@ cudaError_t launch_block_decide(long long* ctl, const unsigned long long* tnext,
     block_decide_kernel<<<1, 1, 0, s>>>(ctl, tnext, tcur, nact, nact_cur, nshards, cond, nodes);
     return cudaGetLastError();
 }
-cudaError_t launch_fill_padding(JPkt* pkt, float4* pklo, JPkt64* pk64, int64_t from, int64_t to,
-                                float eps2, cudaStream_t s) {
+cudaError_t launch_fill_padding(JPkt* pkt, float4* pklo, int64_t from, int64_t to, float eps2, cudaStream_t s) {
     if (to <= from) return cudaSuccess;
-    fill_padding_kernel<<<dims_for(to - from).grid, dims_for(to - from).block, 0, s>>>(pkt, pklo, pk64, from, to, eps2);
+    fill_padding_kernel<<<dims_for(to - from).grid, dims_for(to - from).block, 0, s>>>(pkt, pklo, from, to, eps2);
     return cudaGetLastError();
 }
 

@@ -63,20 +63,12 @@ __device__ __forceinline__ float4 jpkt_pos(const JPkt& k) { return k.p; }   // w
 __device__ __forceinline__ float4 jpkt_vel(const JPkt& k) { return k.v; }   // w = eps2
 #endif
 
-// fp64 j packet for the FP64-pipe share of the force pass (force.cu kHyb):
-// exact fp64 state, (x, y, z, G m) (vx, vy, vz, eps2), 64 B.
-struct __align__(32) JPkt64 {
-    double4 p;
-    double4 v;
-};
-
 constexpr int kTile = 256;  // j per fp32 partial-sum tile (R#10)
 
 // Force pass arguments.  One CTA = (i-block, chunk); see force.cu.
 struct ForceArgs {
     const JPkt* pkt;     // all-gathered j packets [L]
     const float4* pklo;  // NEXT f2 hi/lo: fp32(x - fp32(x)) tails [L], or nullptr
-    const JPkt64* pk64;  // fp64 packets [L] (FP64-pipe i-particles), or nullptr if force_hyb() == 0
     int64_t i_base;      // global index of local particle 0
     int32_t n_loc;       // local particles
     int64_t n_loc_pad;   // row stride of `partial`
@@ -97,6 +89,9 @@ struct ForceArgs {
 // n_chunks) over all local i; jerk == false is the acceleration-only kernel
 // (leapfrog, NEXT f1; partial has 3 components).  Returns the launch error.
 cudaError_t launch_force(const ForceArgs& a, bool guard_self, bool jerk, cudaStream_t s);
+// The same pass pinned to the 1024-i CTA shape (the exchange-overlap launch, sized in
+// whole waves of that shape by the runtime).
+cudaError_t launch_force_big(const ForceArgs& a, bool guard_self, bool jerk, cudaStream_t s);
 int force_i_per_block();
 int force_list_i_per_block(bool big);   // i per CTA of the active-list (block-step) force launches
 // Active-list force pass in the 256-i (big = false) or the 1024-i CTA shape (large active
@@ -111,7 +106,6 @@ int force_tsplit_i_per_block(bool scalar);
 int force_tsplit_threads(int chunk);
 int force_tsplit_max();         // block steps: largest active count for the packed tile-split kernel
 int force_tsplit1_max();        // ... and for the scalar one
-int force_hyb();   // fp64 i-particles per thread in the force kernel (0: pure FP32)
 // resident force CTAs per SM for the kernel variant (occupancy calculator)
 int force_ctas_per_sm(bool jerk, bool hilo);
 
@@ -130,7 +124,6 @@ struct StateArgs {
     int32_t integrator;  // NBODY_HERMITE4 (0) or NBODY_LEAPFROG_KDK (1)
     JPkt* pkt;           // all packets; local particle i goes to pkt[i_base + i]
     float4* pklo;        // hi/lo position tails (nullptr unless hilo)
-    JPkt64* pk64;        // fp64 packets (nullptr unless force_hyb() > 0)
     unsigned long long* bad;  // min global index of a non-finite particle
     // block time steps (NBODY_HERMITE4_BLOCK, R#28); dt above is dt_max
     int64_t* T;          // [n_loc] particle time in ticks of dt_max / 2^kmax
@@ -151,9 +144,10 @@ cudaError_t launch_pack_state(const StateArgs& a, cudaStream_t s);     // x, v -
 cudaError_t launch_predict_pack(const StateArgs& a, cudaStream_t s);   // x,v,a0,j0 -> xp,vp,pkt
 cudaError_t launch_fold_forces(const StateArgs& a, cudaStream_t s);    // partial -> a0, j0
 cudaError_t launch_correct_predict_pack(const StateArgs& a, cudaStream_t s);
-cudaError_t launch_fill_padding(JPkt* pkt, float4* pklo, JPkt64* pk64, int64_t from, int64_t to,
-                                float eps2, cudaStream_t s);
-// bad2[0]: min global index with m not finite or <= 0; bad2[1]: x or v not finite
+cudaError_t launch_fill_padding(JPkt* pkt, float4* pklo, int64_t from, int64_t to, float eps2,
+                                cudaStream_t s);
+// bad2[0]: min global index with m not finite or <= 0; bad2[1]: x or v not finite;
+// bad2[2]: atomicMax of the valid masses' bit patterns (caller zeroes it first)
 cudaError_t launch_validate(const StateArgs& a, unsigned long long* bad2, cudaStream_t s);
 // checkpoint restore: a0, j0 finite (bad2[1] = first bad global index); levels in [0, kmax]
 cudaError_t launch_validate_derivs(const StateArgs& a, unsigned long long* bad2, cudaStream_t s);

@@ -12,11 +12,26 @@
 //
 // NCCL is resolved with dlopen at first use (the libnccl.so.2 the process
 // already loaded, i.e. torch's, unless NBODY_NCCL_LIB names another), so the
-// library never links a second NCCL and never needs one for world == 1.
+// library never links a second NCCL and never needs one for world == 1.  The
+// communicator is non-blocking: every NCCL call is followed by a bounded wait
+// (NBODY_NCCL_TIMEOUT_S) for it to leave ncclInProgress, so a rank that never
+// arrives or dies turns into NBODY_ENCCL instead of a hang, and a failed
+// context is torn down with ncclCommAbort.
+//
+// Loopback mode (cfg.loopback, tests and the scaling projection) runs `world`
+// shards in one context on one GPU.  Each shard owns its exchange buffer, and
+// the all-gather is emulated by one cudaMemcpyAsync per remote slice into it,
+// between the same local-first / remote-second force launches an NCCL rank
+// issues -- so a wrong slice offset or a local launch that reads a remote
+// chunk changes the result (tests/test_gpu_exchange.py).
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <sched.h>
+
+#include <cfloat>
+#include <chrono>
 #include <climits>
 #include <cmath>
 #include <cstdarg>
@@ -41,8 +56,10 @@ struct NcclApi {
     bool tried = false, ok = false;
     std::string why;
     ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
-    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommInitRankConfig)(ncclComm_t*, int, ncclUniqueId, int, ncclConfig_t*) = nullptr;
+    ncclResult_t (*CommFinalize)(ncclComm_t) = nullptr;
     ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*CommAbort)(ncclComm_t) = nullptr;
     ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;
     ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
                               cudaStream_t) = nullptr;
@@ -67,8 +84,10 @@ NcclApi load_nccl() {
         return api;                                                  \
     }
     NB_SYM(GetUniqueId, "ncclGetUniqueId");
-    NB_SYM(CommInitRank, "ncclCommInitRank");
+    NB_SYM(CommInitRankConfig, "ncclCommInitRankConfig");
+    NB_SYM(CommFinalize, "ncclCommFinalize");
     NB_SYM(CommDestroy, "ncclCommDestroy");
+    NB_SYM(CommAbort, "ncclCommAbort");
     NB_SYM(CommGetAsyncError, "ncclCommGetAsyncError");
     NB_SYM(AllGather, "ncclAllGather");
     NB_SYM(AllReduce, "ncclAllReduce");
@@ -117,6 +136,9 @@ int make_plan(int64_t n, int32_t world, int32_t rank, int32_t jchunks, Plan* p, 
 
 struct Shard {
     Plan plan;
+    JPkt* pkt = nullptr;      // exchange buffer this shard packs into and reads j from: the
+    float4* pklo = nullptr;   // context's (NCCL / world 1), or its own (loopback shards >= 1)
+    bool own_pkt = false;
     int32_t n_loc = 0;
     int64_t n_loc_pad = 0;
     double *m = nullptr, *x = nullptr, *v = nullptr, *a0 = nullptr, *j0 = nullptr;
@@ -148,12 +170,13 @@ struct nbody_ctx {
     std::vector<Shard> sh;
     JPkt* pkt = nullptr;
     float4* pklo = nullptr;   // hi/lo position tails (cfg.hilo)
-    nb::JPkt64* pk64 = nullptr;   // fp64 packets for the force kernel's FP64-pipe share
+    bool guard = false;       // eps2f < FLT_MIN (0 or subnormal, flushed to 0 on the device):
+                              // the force pass excludes s == 0 explicitly (R#17)
     double4* eall = nullptr;
     double* eblk = nullptr;
     int eblk_cap = 0;
     double* eout = nullptr;  // [nshards][2]
-    unsigned long long* flags = nullptr;  // [0] non-finite, [1] coincident, [2..3] validate
+    unsigned long long* flags = nullptr;  // [0] non-finite, [1] coincident, [2..4] validate
     // block time steps (R#28): t_next (ticks, shared by all shards), per-shard
     // active counts, pinned read-back of both, run statistics
     unsigned long long* tnext = nullptr;   // this block step's time (ticks)
@@ -166,10 +189,12 @@ struct nbody_ctx {
     void* hbuf = nullptr;
     bool levels_ok = false;
     cudaGraphExec_t block_graph = nullptr;   // WHILE-loop graph of block steps (R#28)
+    bool block_graph_failed = false;         // NCCL ranks: the capture was refused -> host loop
     cudaStream_t stream = nullptr, comm_stream = nullptr;
     bool own_stream = false;
     cudaEvent_t ev_packed = nullptr, ev_gathered = nullptr;
     ncclComm_t comm = nullptr;
+    double nccl_timeout_s = 600.0;
     bool have_a0 = false, predicted = false;
     bool use_graph = true;
     cudaGraphExec_t step_graph = nullptr;
@@ -179,6 +204,7 @@ struct nbody_ctx {
     std::vector<int64_t> prof_ni, prof_nj;   // i and j particles of each timed launch
     size_t prof_used = 0;
     int64_t n_force = 0, n_kernels = 0;
+    int64_t graph_launches = 0, eager_steps = 0;   // nbody_exec_stats
     // block-step graph runs launch their kernels on the device: counted at prof_read time
     // from the block-step counter ctl[1] (minus the host-driven block steps since the reset)
     int64_t block_graph_calls = 0, block_host_steps = 0, block_steps_at_reset = 0;
@@ -210,11 +236,32 @@ int fail(nbody_ctx* c, int code, const char* fmt, ...) {
                         cudaGetErrorString(e_), __FILE__, __LINE__);                       \
     } while (0)
 
+// Non-blocking communicator: a call returns ncclSuccess or ncclInProgress, and the next
+// call may only be issued once the communicator has left ncclInProgress.  Wait for
+// that, at most c->nccl_timeout_s seconds (then NBODY_ENCCL, and the context is torn
+// down with ncclCommAbort).
+int nccl_settle(nbody_ctx* c, ncclResult_t r, const char* what) {
+    if (r != ncclSuccess && r != ncclInProgress)
+        return fail(c, NBODY_ENCCL, "%s failed: %s", what, nccl().GetErrorString(r));
+    const auto t0 = std::chrono::steady_clock::now();
+    for (int spin = 0;; ++spin) {
+        ncclResult_t st = ncclSuccess;
+        ncclResult_t q = nccl().CommGetAsyncError(c->comm, &st);
+        if (q != ncclSuccess) return fail(c, NBODY_ENCCL, "%s: ncclCommGetAsyncError: %s", what, nccl().GetErrorString(q));
+        if (st == ncclSuccess) return NBODY_OK;
+        if (st != ncclInProgress) return fail(c, NBODY_ENCCL, "%s: %s", what, nccl().GetErrorString(st));
+        const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        if (el > c->nccl_timeout_s)
+            return fail(c, NBODY_ENCCL, "%s: no progress after %.1f s (NBODY_NCCL_TIMEOUT_S); a peer rank "
+                        "is missing or dead", what, el);
+        if (spin > 64) sched_yield();
+    }
+}
+
 #define CKNCCL(ctx, call)                                                                  \
     do {                                                                                   \
-        ncclResult_t r_ = (call);                                                          \
-        if (r_ != ncclSuccess)                                                             \
-            return fail(ctx, NBODY_ENCCL, "%s failed: %s", #call, nccl().GetErrorString(r_)); \
+        int rc_ = nccl_settle(ctx, (call), #call);                                         \
+        if (rc_) return rc_;                                                               \
     } while (0)
 
 #define GUARD(ctx)                                                                          \
@@ -242,9 +289,8 @@ nb::StateArgs state_args(nbody_ctx* c, Shard& s) {
     a.n_chunks = (int32_t)s.plan.n_chunks;
     a.ncomp = ncomp(c);
     a.integrator = c->cfg.integrator == NBODY_LEAPFROG_KDK ? 1 : 0;   // predictor/corrector family
-    a.pkt = c->pkt;
-    a.pklo = c->pklo;
-    a.pk64 = c->pk64;
+    a.pkt = s.pkt;
+    a.pklo = s.pklo;
     a.bad = c->flags;
     a.T = s.T;
     a.lev = s.lev;
@@ -267,15 +313,16 @@ bool use_nccl(const nbody_ctx* c) { return c->comm != nullptr; }
 // force pass over chunks [c_first, c_first + c_count) for the shard's local
 // particles, or (block steps) for the n_i active particles listed in ilist
 // tsplit (block steps): 0 = list kernel (256-i CTAs), 1 = packed tile-split, 2 = scalar
-// tile-split, 3 = list kernel (1024-i CTAs); plain launches: 0
+// tile-split, 3 = list kernel (1024-i CTAs); plain launches: 0 (CTA shape by size) or
+// kForceBig (1024-i CTAs: the exchange-overlap launch, sized in whole waves of that shape)
+constexpr int kForceBig = 4;
 int launch_force_range(nbody_ctx* c, Shard& s, int32_t c_first, int32_t c_count, int32_t n_i = -1,
                        const int32_t* ilist = nullptr, const int32_t* n_dev = nullptr, int tsplit = 0) {
     if (n_i < 0) n_i = s.n_loc;
     if (c_count <= 0 || n_i <= 0) return NBODY_OK;
     nb::ForceArgs f;
-    f.pkt = c->pkt;
-    f.pklo = c->pklo;
-    f.pk64 = c->pk64;
+    f.pkt = s.pkt;
+    f.pklo = s.pklo;
     f.i_base = s.plan.i0;
     f.n_loc = n_i;
     f.ilist = ilist;
@@ -312,40 +359,77 @@ int launch_force_range(nbody_ctx* c, Shard& s, int32_t c_first, int32_t c_count,
         CK(c, cudaEventRecord(e0, c->stream));
     }
     if (tsplit == 1 || tsplit == 2)
-        CK(c, nb::launch_force_tsplit(f, c->eps2f == 0.f, ncomp(c) == 6, tsplit == 2, c->stream));
+        CK(c, nb::launch_force_tsplit(f, c->guard, ncomp(c) == 6, tsplit == 2, c->stream));
     else if (ilist)
-        CK(c, nb::launch_force_list(f, c->eps2f == 0.f, tsplit == 3, c->stream));
+        CK(c, nb::launch_force_list(f, c->guard, tsplit == 3, c->stream));
+    else if (tsplit == kForceBig)
+        CK(c, nb::launch_force_big(f, c->guard, ncomp(c) == 6, c->stream));
     else
-        CK(c, nb::launch_force(f, c->eps2f == 0.f, ncomp(c) == 6, c->stream));
+        CK(c, nb::launch_force(f, c->guard, ncomp(c) == 6, c->stream));
     if (e1) CK(c, cudaEventRecord(e1, c->stream));
     c->n_force++;
     c->n_kernels++;
     return NBODY_OK;
 }
 
-// exchange the packets written by every shard's pack kernel, then run the
-// force pass of every shard: local chunks first (overlapping the
-// all-gather), remote chunks after it.
-// in-place all-gather of every rank's packet slice (and hi/lo tails, fp64
-// packets when present) on stream st
+// ---- exchange (a2).  Rank r's slice of the exchange buffer holds particles
+// [r * slot, (r + 1) * slot) (R#22); both back ends address slices through these two.
+// NB_TEST_MUTATE (never set in the product build): deliberately wrong variants that
+// tests/test_gpu_exchange.py builds to show the exchange tests detect them --
+// 1: slices permuted (rank r addressed at (r + 1) mod world), 2: the local-first launch
+// starts at chunk 0 instead of the rank's first local chunk.
+#ifndef NB_TEST_MUTATE
+#define NB_TEST_MUTATE 0
+#endif
+size_t slice_begin(const nbody_ctx* c, int r) {
+    if (NB_TEST_MUTATE == 1) r = (r + 1) % c->cfg.world;
+    return (size_t)r * (size_t)c->sh[0].plan.slot;
+}
+size_t slice_len(const nbody_ctx* c) { return (size_t)c->sh[0].plan.slot; }
+
+// NCCL: in-place all-gather of every rank's packet slice (and hi/lo tails) on stream st
 int gather_packets(nbody_ctx* c, cudaStream_t st) {
-    Shard& s = c->sh[0];
+    const size_t off = slice_begin(c, c->cfg.rank), len = slice_len(c);
+    constexpr size_t kPf = sizeof(JPkt) / sizeof(float), kLf = sizeof(float4) / sizeof(float);
     float* base = reinterpret_cast<float*>(c->pkt);
-    const size_t cnt = (size_t)s.plan.slot * (sizeof(JPkt) / sizeof(float));
-    CKNCCL(c, nccl().AllGather(base + (size_t)c->cfg.rank * cnt, base, cnt, ncclFloat32, c->comm, st));
+    CKNCCL(c, nccl().AllGather(base + off * kPf, base, len * kPf, ncclFloat32, c->comm, st));
     if (c->pklo) {
         float* lo = reinterpret_cast<float*>(c->pklo);
-        const size_t cl = (size_t)s.plan.slot * 4;
-        CKNCCL(c, nccl().AllGather(lo + (size_t)c->cfg.rank * cl, lo, cl, ncclFloat32, c->comm, st));
-    }
-    if (c->pk64) {
-        double* d64 = reinterpret_cast<double*>(c->pk64);
-        const size_t c8 = (size_t)s.plan.slot * 8;
-        CKNCCL(c, nccl().AllGather(d64 + (size_t)c->cfg.rank * c8, d64, c8, ncclFloat64, c->comm, st));
+        CKNCCL(c, nccl().AllGather(lo + off * kLf, lo, len * kLf, ncclFloat32, c->comm, st));
     }
     return NBODY_OK;
 }
 
+// loopback: what the all-gather delivers to shard q -- every other shard's slice, copied
+// from that shard's own buffer into q's, one cudaMemcpyAsync per slice
+int gather_into(nbody_ctx* c, int q, cudaStream_t st) {
+    const size_t len = slice_len(c);
+    Shard& d = c->sh[q];
+    for (int r = 0; r < c->nshards; ++r) {
+        if (r == q) continue;
+        const size_t off = slice_begin(c, r);
+        CK(c, cudaMemcpyAsync(d.pkt + off, c->sh[r].pkt + off, len * sizeof(JPkt), cudaMemcpyDeviceToDevice, st));
+        if (d.pklo)
+            CK(c, cudaMemcpyAsync(d.pklo + off, c->sh[r].pklo + off, len * sizeof(float4),
+                                  cudaMemcpyDeviceToDevice, st));
+    }
+    return NBODY_OK;
+}
+
+// Chunks of the local-first force launch that overlaps the exchange: one wave of
+// (i-block x chunk) work items in the 1024-i CTA shape the launch is pinned to (a
+// partial wave would idle SMs until it drains, costing more than the ~10 us gather);
+// fewer when the rank has fewer local chunks.  Results do not depend on it.
+int32_t overlap_chunks(const nbody_ctx* c, const Shard& s) {
+    const int32_t nl = s.c_hi - s.c_lo;
+    const int64_t n_ib = (s.n_loc + nb::force_i_per_block() - 1) / nb::force_i_per_block();
+    if (nl <= 0 || n_ib <= 0) return 0;
+    const int64_t slots = (int64_t)c->sm_count * nb::force_ctas_per_sm(ncomp(c) == 6, s.pklo != nullptr);
+    return (int32_t)std::min<int64_t>(nl, std::max<int64_t>(1, slots / n_ib));
+}
+
+// exchange the packets every shard's pack kernel wrote and run every shard's force pass:
+// local chunks first (overlapping the exchange), the remaining chunks after it
 int exchange_and_force(nbody_ctx* c) {
     int rc;
     if (use_nccl(c)) {
@@ -354,27 +438,23 @@ int exchange_and_force(nbody_ctx* c) {
         CK(c, cudaStreamWaitEvent(c->comm_stream, c->ev_packed, 0));
         if ((rc = gather_packets(c, c->comm_stream))) return rc;
         CK(c, cudaEventRecord(c->ev_gathered, c->comm_stream));
-        // Overlap: while the all-gather runs, compute a whole number of waves of
-        // local-chunk work items (i-block x chunk) -- a partial wave here would
-        // idle SMs until the launch drains, costing more than the ~10 us gather.
-        // Everything else (remaining local + all remote chunks) runs as one grid
-        // after the gather.  Results do not depend on this split.
-        const int32_t nl = s.c_hi - s.c_lo;
-        const int64_t n_ib = (s.n_loc + nb::force_i_per_block() - 1) / nb::force_i_per_block();
-        int32_t f = 0;
-        if (nl > 0 && n_ib > 0) {
-            const int64_t slots = (int64_t)c->sm_count * nb::force_ctas_per_sm(
-                                      c->cfg.integrator == NBODY_HERMITE4, c->pklo != nullptr);
-            f = (int32_t)std::min<int64_t>(nl, std::max<int64_t>(1, slots / n_ib));   // <= 1 wave
-        }
-        if ((rc = launch_force_range(c, s, s.c_lo, f))) return rc;
+        const int32_t f = overlap_chunks(c, s), nch = (int32_t)s.plan.n_chunks;
+        if ((rc = launch_force_range(c, s, s.c_lo, f, -1, nullptr, nullptr, kForceBig))) return rc;
         CK(c, cudaStreamWaitEvent(c->stream, c->ev_gathered, 0));
-        const int32_t nch = (int32_t)s.plan.n_chunks;
         if ((rc = launch_force_range(c, s, (s.c_lo + f) % nch, nch - f))) return rc;
+    } else if (c->nshards > 1) {
+        // loopback: per shard the same two launches, the emulated gather between them
+        for (int q = 0; q < c->nshards; ++q) {
+            Shard& s = c->sh[q];
+            const int32_t f = overlap_chunks(c, s), nch = (int32_t)s.plan.n_chunks;
+            const int32_t c0 = NB_TEST_MUTATE == 2 ? 0 : s.c_lo;
+            if ((rc = launch_force_range(c, s, c0, f, -1, nullptr, nullptr, kForceBig))) return rc;
+            if ((rc = gather_into(c, q, c->stream))) return rc;
+            if ((rc = launch_force_range(c, s, (c0 + f) % nch, nch - f))) return rc;
+        }
     } else {
-        // world == 1 or loopback: every packet already sits in c->pkt
-        for (auto& s : c->sh)
-            if ((rc = launch_force_range(c, s, 0, (int32_t)s.plan.n_chunks))) return rc;
+        Shard& s = c->sh[0];   // world == 1: every packet already sits in the buffer
+        if ((rc = launch_force_range(c, s, 0, (int32_t)s.plan.n_chunks))) return rc;
     }
     return NBODY_OK;
 }
@@ -439,8 +519,21 @@ void free_ctx(nbody_ctx* c) {
     cudaSetDevice(c->cfg.device);
     if (c->stream) cudaStreamSynchronize(c->stream);
     if (c->step_graph) cudaGraphExecDestroy(c->step_graph);
-    if (c->comm && nccl().ok) nccl().CommDestroy(c->comm);
+    if (c->comm && nccl().ok) {
+        // a failed context (or a peer that never arrives) must not block here: abort it;
+        // a healthy one is finalized (bounded wait) and destroyed
+        bool abort = c->sticky != 0;
+        if (!abort) {
+            const std::string err = c->err;
+            abort = nccl_settle(c, nccl().CommFinalize(c->comm), "ncclCommFinalize") != NBODY_OK;
+            if (!abort) c->err = err;
+        }
+        if (abort) nccl().CommAbort(c->comm);
+        else nccl().CommDestroy(c->comm);
+        c->comm = nullptr;
+    }
     for (auto& s : c->sh) {
+        if (s.own_pkt) { cudaFree(s.pkt); cudaFree(s.pklo); }
         cudaFree(s.m); cudaFree(s.x); cudaFree(s.v); cudaFree(s.a0); cudaFree(s.j0);
         cudaFree(s.xp); cudaFree(s.vp); cudaFree(s.partial);
         cudaFree(s.T); cudaFree(s.lev); cudaFree(s.ilist);
@@ -456,7 +549,6 @@ void free_ctx(nbody_ctx* c) {
     if (c->hbuf) cudaFreeHost(c->hbuf);
     cudaFree(c->pkt);
     cudaFree(c->pklo);
-    cudaFree(c->pk64);
     cudaFree(c->eall);
     cudaFree(c->eblk);
     cudaFree(c->eout);
@@ -507,6 +599,8 @@ int init_impl(const nbody_config* cfg, const double* m, const double* x, const d
     const char* ng = getenv("NBODY_NO_GRAPH");
     c->use_graph = !(ng && *ng && *ng != '0');
     c->eps2f = (float)(k.eps * k.eps);
+    c->guard = c->eps2f < FLT_MIN;   // 0, or subnormal (flushed to 0 by the FTZ force pass)
+    if (const char* t = getenv("NBODY_NCCL_TIMEOUT_S"); t && *t && atof(t) > 0) c->nccl_timeout_s = atof(t);
     c->nshards = k.loopback ? k.world : 1;
     c->sh.resize(c->nshards);
     std::string why;
@@ -532,8 +626,18 @@ int init_impl(const nbody_config* cfg, const double* m, const double* x, const d
 
     if ((rc = dalloc(c, &c->pkt, (size_t)c->L))) return rc;
     if (k.hilo && (rc = dalloc(c, &c->pklo, (size_t)c->L))) return rc;
-    if (nb::force_hyb() > 0 && (rc = dalloc(c, &c->pk64, (size_t)c->L))) return rc;
-    if ((rc = dalloc(c, &c->flags, 4))) return rc;
+    for (int q = 0; q < c->nshards; ++q) {
+        Shard& s = c->sh[q];
+        if (q == 0) {
+            s.pkt = c->pkt;
+            s.pklo = c->pklo;
+            continue;
+        }
+        s.own_pkt = true;   // loopback: every shard packs into and reads from its own buffer
+        if ((rc = dalloc(c, &s.pkt, (size_t)c->L))) return rc;
+        if (k.hilo && (rc = dalloc(c, &s.pklo, (size_t)c->L))) return rc;
+    }
+    if ((rc = dalloc(c, &c->flags, 5))) return rc;
     if (is_block(c)) {
         if ((rc = dalloc(c, &c->tnext, 1)) || (rc = dalloc(c, &c->tcur, 1)) ||
             (rc = dalloc(c, &c->nact, (size_t)c->nshards)) || (rc = dalloc(c, &c->nact_cur, (size_t)c->nshards)) ||
@@ -544,8 +648,11 @@ int init_impl(const nbody_config* cfg, const double* m, const double* x, const d
         CK(c, cudaMallocHost(&c->hbuf, 8 + 4 * (size_t)c->nshards));
     }
     CK(c, cudaMemsetAsync(c->flags, 0xff, 4 * sizeof(unsigned long long), c->stream));
-    CK(c, nb::launch_fill_padding(c->pkt, c->pklo, c->pk64, 0, c->L, c->eps2f, c->stream));
-    c->n_kernels++;
+    CK(c, cudaMemsetAsync(c->flags + 4, 0, sizeof(unsigned long long), c->stream));
+    for (auto& s : c->sh) {
+        CK(c, nb::launch_fill_padding(s.pkt, s.pklo, 0, c->L, c->eps2f, c->stream));
+        c->n_kernels++;
+    }
 
     const int64_t ib = nb::force_i_per_block();
     for (auto& s : c->sh) {
@@ -579,18 +686,30 @@ int init_impl(const nbody_config* cfg, const double* m, const double* x, const d
         CK(c, nb::launch_validate(state_args(c, s), c->flags + 2, c->stream));
         c->n_kernels++;
     }
-    unsigned long long bad[2];
+    unsigned long long bad[3];
     CK(c, cudaMemcpyAsync(bad, c->flags + 2, sizeof bad, cudaMemcpyDeviceToHost, c->stream));
     CK(c, cudaStreamSynchronize(c->stream));
     if (bad[0] != ULLONG_MAX) return fail(c, NBODY_EINVAL, "mass of particle %llu is not finite and > 0", bad[0]);
     if (bad[1] != ULLONG_MAX) return fail(c, NBODY_EINVAL, "position or velocity of particle %llu is not finite", bad[1]);
+    // fp32 range of the pair terms: G m_j / s^{3/2} <= G max(m) / eps^3 must stay far below
+    // FLT_MAX (1e30 leaves 8 decades for |v|, the jerk terms and the tile sums); with
+    // eps = 0 a pair closer than that range allows is reported as non-finite instead
+    double mmax = 0;
+    memcpy(&mmax, &bad[2], sizeof mmax);
+    if (k.eps > 0 && k.G * mmax / (k.eps * k.eps * k.eps) > 1e30)
+        return fail(c, NBODY_EINVAL, "G max(m) / eps^3 = %.3g exceeds the fp32 range of the force pass "
+                    "(limit 1e30): increase eps", k.G * mmax / (k.eps * k.eps * k.eps));
 
     if (k.nccl_id && !k.loopback) {
         NcclApi& api = nccl();
         if (!api.ok) return fail(c, NBODY_ENCCL, "%s", api.why.c_str());
         ncclUniqueId id;
         memcpy(id.internal, k.nccl_id, NCCL_UNIQUE_ID_BYTES);
-        CKNCCL(c, api.CommInitRank(&c->comm, k.world, id, k.rank));
+        ncclConfig_t nc = NCCL_CONFIG_INITIALIZER;
+        nc.blocking = 0;   // bounded waits (nccl_settle), abortable
+        ncclResult_t r = api.CommInitRankConfig(&c->comm, k.world, id, k.rank, &nc);
+        if (r != ncclSuccess && r != ncclInProgress) c->comm = nullptr;   // nothing to abort
+        CKNCCL(c, r);
     }
     return NBODY_OK;
 }
@@ -757,6 +876,8 @@ int capture_force_node(nbody_ctx* c, cudaGraphDeviceNode_t* out) {
 int block_step_rest(nbody_ctx* c, const int32_t* n_act, nb::BlockGraphNodes* nodes) {
     int rc;
     if (use_nccl(c) && (rc = gather_packets(c, c->stream))) return rc;
+    for (int q = 0; c->nshards > 1 && q < c->nshards; ++q)
+        if ((rc = gather_into(c, q, c->stream))) return rc;
     for (int q = 0; q < c->nshards; ++q) {
         Shard& s = c->sh[q];
         const int32_t n_i = n_act ? n_act[q] : std::max<int32_t>(1, s.n_loc);
@@ -795,6 +916,7 @@ int block_step_rest(nbody_ctx* c, const int32_t* n_act, nb::BlockGraphNodes* nod
     return NBODY_OK;
 }
 
+int block_run_host(nbody_ctx* c);
 int block_run(nbody_ctx* c, int32_t nsteps) {
     int rc;
     const int kmax = c->cfg.kmax;
@@ -812,7 +934,10 @@ int block_run(nbody_ctx* c, int32_t nsteps) {
     c->levels_ok = true;
     CK(c, nb::launch_block_set_tend(c->ctl, (unsigned long long)nsteps << kmax, c->stream));
     CK(c, nb::launch_block_begin(c->tcur, c->nact, c->nshards, c->stream));
-    const bool graph_ok = !use_nccl(c) && !c->prof && c->use_graph && c->nshards <= 8 &&
+    // NCCL ranks capture the t_next all-reduce and the packet all-gather into the WHILE body
+    // too (every rank runs the same number of iterations: done derives from the reduced
+    // t_next); if the runtime refuses that capture the host-driven loop is used instead
+    const bool graph_ok = !c->block_graph_failed && !c->prof && c->use_graph && c->nshards <= 8 &&
                           c->stream != cudaStreamLegacy && c->stream != cudaStreamPerThread &&
                           c->stream != nullptr;
     if (graph_ok) {
@@ -852,22 +977,31 @@ int block_run(nbody_ctx* c, int32_t nsteps) {
             e = cudaStreamEndCapture(c->stream, &body);
             c->n_kernels = nk0;
             c->n_force = nf0;
-            if (rc || e != cudaSuccess) {
-                cudaGraphDestroy(g);
-                if (rc) return rc;
-                CK(c, e);
-            }
-            e = cudaGraphInstantiate(&c->block_graph, g, 0);
+            if (!rc && e == cudaSuccess) e = cudaGraphInstantiate(&c->block_graph, g, 0);
             cudaGraphDestroy(g);
+            if (rc) return rc;
+            if (e != cudaSuccess && use_nccl(c)) {
+                cudaGetLastError();
+                c->block_graph = nullptr;
+                c->block_graph_failed = true;   // fall through to the host-driven loop
+                return block_run_host(c);
+            }
             CK(c, e);
             CK(c, cudaMemcpyAsync(c->gnodes, &hn, sizeof hn, cudaMemcpyHostToDevice, c->stream));
             CK(c, cudaStreamSynchronize(c->stream));   // hn is a stack object
         }
         CK(c, cudaGraphLaunch(c->block_graph, c->stream));
         c->block_graph_calls++;
+        c->graph_launches++;
         return NBODY_OK;
     }
-    // host-driven loop (NCCL ranks, kernel timing, no capturable stream)
+    return block_run_host(c);
+}
+
+// host-driven block-step loop (kernel timing, no capturable stream, or an NCCL capture the
+// runtime refused): one host round trip per block step
+int block_run_host(nbody_ctx* c) {
+    int rc;
     long long* h_done = reinterpret_cast<long long*>(c->hbuf);
     int32_t* h_nact = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(c->hbuf) + 8);
     for (;;) {
@@ -878,6 +1012,7 @@ int block_run(nbody_ctx* c, int32_t nsteps) {
         if (*h_done) break;
         if ((rc = block_step_rest(c, h_nact, nullptr))) return rc;
         c->block_host_steps++;
+        c->eager_steps++;
     }
     return NBODY_OK;
 }
@@ -921,8 +1056,10 @@ int nbody_step(nbody_ctx* c, int32_t nsteps) {
             CK(c, cudaGraphLaunch(c->step_graph, c->stream));
             c->n_kernels += c->graph_kernels;
             c->n_force += c->graph_force;
-        } else if ((rc = one_step(c))) {
-            return rc;
+            c->graph_launches++;
+        } else {
+            if ((rc = one_step(c))) return rc;
+            c->eager_steps++;
         }
     }
     return NBODY_OK;
@@ -1163,6 +1300,13 @@ int nbody_prof_launch_sizes(nbody_ctx* c, int64_t* n_i, int64_t* n_j, int64_t ca
         if (n_j) n_j[q] = c->prof_nj[q];
     }
     if (count) *count = nrec;
+    return NBODY_OK;
+}
+
+int nbody_exec_stats(const nbody_ctx* c, int64_t* graph_launches, int64_t* eager_steps) {
+    if (!c) return fail(nullptr, NBODY_EINVAL, "null context");
+    if (graph_launches) *graph_launches = c->graph_launches;
+    if (eager_steps) *eager_steps = c->eager_steps;
     return NBODY_OK;
 }
 

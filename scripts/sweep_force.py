@@ -15,22 +15,17 @@ sys.path.insert(0, ROOT)
 OUT = os.path.join(ROOT, "scripts", "sweep")
 
 VARIANTS = {
-    # the variants measured so far are recorded in profiles/r01_sweep_force.txt; the
-    # register-prefetch and per-warp empty-barrier ring experiments were removed from
-    # force.cu after measuring slower
-    "base":      dict(),
-    "st3":       dict(FK_STAGES=3),
-    "b3u1":      dict(FK_MINB=3, FK_UNROLL=1),
-    "t64b4":     dict(FK_THREADS=64, FK_MINB=4),
-    "p3b3":      dict(FK_PAIRS=3, FK_MINB=3),
-    "t160":      dict(FK_THREADS=160),              # 10 warps per SM (3/3/2/2 per SMSP)
-    "t96b3":     dict(FK_THREADS=96, FK_MINB=3),   # 9 warps per SM
-    "ptxO1":     dict(_FLAGS=("-Xptxas", "-O1")),   # ptxas optimisation level (schedule)
-    "ptxO2":     dict(_FLAGS=("-Xptxas", "-O2")),
-    "b1":        dict(FK_MINB=1),
-    "b1u3":      dict(FK_MINB=1, FK_UNROLL=3),
-    "b1u4":      dict(FK_MINB=1, FK_UNROLL=4),
-
+    # round-1 variants (3-stage ring, 3 CTAs/SM, 64/96/160 threads, 3 pairs, ptxas -O1/-O2,
+    # 1 CTA/SM with unroll 3/4) are recorded in profiles/r01_sweep_force.txt; round 2
+    # sweeps the software-pipelined j loop (FK_PIPE, profiles/r02_sweep_force.txt)
+    "base":      dict(FK_PIPE=0),
+    "pipe":      dict(FK_PIPE=1),
+    "pipe_u1":   dict(FK_PIPE=1, FK_UNROLL=1),
+    "pipe_u4":   dict(FK_PIPE=1, FK_UNROLL=4),
+    "pp":        dict(FK_PIPE=2),
+    "pipe_p3b3": dict(FK_PIPE=1, FK_PAIRS=3, FK_MINB=3),
+    "pp_p3b3":   dict(FK_PIPE=2, FK_PAIRS=3, FK_MINB=3),
+    "pipe_st3":  dict(FK_PIPE=1, FK_STAGES=3),
 }
 if os.environ.get("SWEEP_ONLY"):
     VARIANTS = {k: v for k, v in VARIANTS.items() if k in os.environ["SWEEP_ONLY"].split(",")}

@@ -66,6 +66,53 @@ def test_force_kernel_uses_packed_fp32x2_and_bulk_tma():
         assert "HMMA" not in b and "UTCHMMA" not in b   # no tensor cores: not a contraction
 
 
+def _sass_loops(block):
+    """(opcode histogram, body) of every backward-branch loop in one SASS function."""
+    import collections
+    ins = []
+    for ln in block.split("\n"):
+        m = re.match(r"\s+/\*([0-9a-f]{4,})\*/\s+(.*?);", ln)
+        if m:
+            ins.append((int(m.group(1), 16), m.group(2).strip()))
+    at = {a: k for k, (a, _) in enumerate(ins)}
+    loops = []
+    for k, (a, t) in enumerate(ins):
+        m = re.search(r"BRA(?:\.U)?(?:\.ANY)? (?:!?U?P\w+, )?0x([0-9a-f]+)", t)
+        if m and int(m.group(1), 16) < a and int(m.group(1), 16) in at:
+            body = [x for _, x in ins[at[int(m.group(1), 16)]:k + 1]]
+            ops = collections.Counter((x.split()[1] if x.startswith("@") else x.split()[0]).split(".")[0]
+                                      for x in body)
+            loops.append(ops)
+    return loops
+
+
+# FP32 instructions per packed i-pair and j (DESIGN.md R#20): acceleration + jerk 26
+# (7 FFMA2 + 3 FMUL2 + ... = 40 flops per interaction), acceleration only 12 (18 flops),
+# hi/lo positions + 6 FADD2; 2 MUFU.RSQ (one per lane) in every form.
+@pytest.mark.parametrize("jerk,hilo,packed", [(1, 0, 26), (0, 0, 12), (1, 1, 32), (0, 1, 18)])
+def test_force_hot_loop_instruction_histogram(jerk, hilo, packed):
+    """SASS opcode count of the 1024-i CTA shape's j loop: per i-pair and j
+    exactly `packed` FFMA2/FADD2/FMUL2 and 2 MUFU.RSQ, no scalar FP32 arithmetic, no
+    FP64 and no tensor-core instruction -- a regression that adds scalar FMULs, splits a
+    packed op or leaves a conversion in the loop fails here."""
+    import subprocess
+    from paper_2509_19294_b200 import _build
+    sass = subprocess.run(["cuobjdump", "-sass", _build.LIB], capture_output=True, text=True).stdout
+    blocks = re.split(r"\n\s*Function : ", sass)
+    # force_kernel<guard = false, jerk, hilo, CfgBig (4 pairs x 128 threads), list = false>
+    pat = re.compile(rf"force_kernelILb0ELb{jerk}ELb{hilo}ENS0_5FkCfgILi4ELi128E.*ELb0EEEvNS_9ForceArgsE")
+    fn = [b for b in blocks if pat.search(b.split("\n")[0])]
+    assert len(fn) == 1, [b.split("\n")[0] for b in fn]
+    loops = _sass_loops(fn[0])
+    hot = min((c for c in loops if c["MUFU"]), key=lambda c: sum(c.values()))   # innermost j loop
+    pairs = 4
+    nj = hot["MUFU"] / (2 * pairs)          # j interactions per loop iteration
+    assert nj >= 1 and nj == int(nj), hot
+    assert hot["FFMA2"] + hot["FADD2"] + hot["FMUL2"] == packed * pairs * nj, hot
+    for op in ("FFMA", "FADD", "FMUL", "DFMA", "DADD", "DMUL", "F2F", "HMMA", "UTCHMMA"):
+        assert hot[op] == 0, (op, hot)
+
+
 @pytest.mark.parametrize("n,world", [(2, 1), (1000, 3), (1024, 4), (262144, 8), (1048576, 8),
                                      (131072, 2), (12345, 7)])
 def test_plan_partition_covers_all_particles(n, world):

@@ -196,13 +196,35 @@ def test_force_cta_shapes_bit_identical(n, monkeypatch):
 
 def test_block_nccl_single_rank_communicator():
     """world = 1 with an NCCL id runs the multi-rank block path for real: t_next through
-    ncclAllReduce(min), packets through ncclAllGather (in place).  Same schedule and
-    bit-identical states as the communicator-free path."""
+    ncclAllReduce(min), packets through ncclAllGather (in place).  On a capturable stream
+    both collectives are captured into the block-step WHILE graph (one graph launch per
+    nbody_step, no host round trip per block step); with kernel timing on, the host drives
+    the same kernels block step by block step.  Same schedule and bit-identical states as
+    the communicator-free path in all three."""
     m, x, v = inputs.parity_round(*inputs.plummer(5000, 9))
-    plain = run_block(m, x, v, 1e-3, 1 / 128, 2)
-    nccl = run_block(m, x, v, 1e-3, 1 / 128, 2, nccl_id=binding.nccl_unique_id())
-    assert np.array_equal(plain[0], nccl[0]) and np.array_equal(plain[1], nccl[1])
-    assert np.array_equal(plain[2], nccl[2]) and plain[3] == nccl[3]
+    st = torch.cuda.Stream()
+    plain = run_block(m, x, v, 1e-3, 1 / 128, 2, stream=st)
+
+    def run_nccl(prof):
+        with binding.NBody(m, x, v, eps=1e-3, dt=1 / 128, integrator="block", stream=st,
+                           nccl_id=binding.nccl_unique_id()) as s:
+            if prof:
+                s.prof_enable(True)
+            s.step(1)
+            s.step(1)
+            xs, vs = s.state()
+            steps, active, lev = s.block_stats(levels=True)
+            s.sync()
+            return (xs.cpu().numpy(), vs.cpu().numpy(), lev, (steps, active)), s.exec_stats()
+
+    for prof in (False, True):
+        got, (graphs, eager) = run_nccl(prof)
+        assert np.array_equal(plain[0], got[0]) and np.array_equal(plain[1], got[1]), prof
+        assert np.array_equal(plain[2], got[2]) and plain[3] == got[3], prof
+        if prof:
+            assert graphs == 0 and eager == plain[3][0]
+        else:
+            assert graphs == 2 and eager == 0   # both calls ran as one WHILE-graph launch each
 
 
 def test_block_kmax_cap_and_compute_forces_mid_run():

@@ -1,6 +1,7 @@
 """Randomised GPU parity sweep through the C-ABI: seeded random system sizes, softenings,
 shard counts, position modes and integrators, each checked against the fp64 oracle and
 against the unsharded run.  The seeds are fixed, so a failure is reproducible."""
+import math
 import os
 
 import numpy as np
@@ -99,12 +100,22 @@ def test_random_block_case(k, monkeypatch):
     assert np.isfinite(ref[0]).all() and np.isfinite(ref[1]).all()
     if n <= 1025 and hilo:   # oracle schedule parity needs two-float positions (R#28)
         e2 = float(np.float32(eps * eps))
-        xo, vo, _, _, lo, so, co = oracle.hermite_block(m, x, v, e2, dt_max, 1, eta=eta, eta_s=0.01,
-                                                        kmax=20)
-        # force evaluations are the robust schedule statistic; the block-step count is not
-        # (one particle on the adjacent, also valid, finer level near a boundary adds block
-        # steps with tiny active sets -- see test_block_c4_schedule_and_state_vs_oracle)
-        assert abs(ref[3][1] - so[1]) <= 0.02 * so[1] + 8, (k, ref[3], so)
-        assert ref[3][0] <= 2 * so[0] + 8 and so[0] <= 2 * ref[3][0] + 8, (k, ref[3], so)
+        xo, vo, _, _, lo, so, co, mg = oracle.hermite_block(m, x, v, e2, dt_max, 1, eta=eta, eta_s=0.01,
+                                                            kmax=20, margin=True)
+        # Schedule differences are attributed, particle by particle, to level decisions the
+        # oracle itself took within round-off of a power-of-two boundary (R#28): mg is the
+        # smallest distance of log2(dt_max / dt_c) to an integer over each particle's
+        # decisions, and 1e-3 / ln 2 (a relative 1e-3 change of dt_c, ~100x the GPU's fp32
+        # force error) is the margin test_gpu_block's _levels_agree uses.
+        near = mg < 1e-3 / math.log(2)
+        lg = ref[2]
+        assert np.array_equal(lg[~near], lo[~near]), (k, np.flatnonzero((lg != lo) & ~near)[:10])
+        assert np.all(np.abs(lg - lo) <= 1), k
+        # a particle flipping between levels k and k + 1 adds at most its own 2^(k+1) step
+        # times (block steps) and evaluations per dt_max; without such a particle the counts
+        # agree to 5 % (block steps) / 2 % (force evaluations)
+        slack = int(sum(2 ** (1 + max(int(lg[i]), int(lo[i]))) for i in np.flatnonzero(near)))
+        assert abs(ref[3][0] - so[0]) <= 0.05 * so[0] + 2 + slack, (k, ref[3], so, int(near.sum()))
+        assert abs(ref[3][1] - so[1]) <= 0.02 * so[1] + 2 + slack, (k, ref[3], so, int(near.sum()))
         # positions agree to the level of a few adjacent-level choices (see test_gpu_block)
         assert np.max(np.abs(ref[0] - xo)) <= 1e-6, (k, np.max(np.abs(ref[0] - xo)))
