@@ -64,7 +64,7 @@ def _load():
     lib.oracle_block_init_levels.argtypes = [i64, d, i32, d, p, p, p, p]
     lib.oracle_block_init_levels.restype = ctypes.c_int
     lib.oracle_hermite_block.argtypes = [i64, d, d, d, i32, d, d, i64, p, p, p, p, p, p, i32, p, p,
-                                         p, p, p]
+                                         p, p]
     lib.oracle_hermite_block.restype = ctypes.c_int
     lib.oracle_threads.argtypes = []
     lib.oracle_threads.restype = ctypes.c_int
@@ -201,16 +201,14 @@ def block_init_levels(acc, jerk, dt_max: float, kmax: int, eta_s: float):
 
 def hermite_block(m, x, v, eps2: float, dt_max: float, ncycles: int, eta: float,
                   eta_s: float = 0.01, kmax: int = 20, G: float = 1.0, acc=None, jerk=None,
-                  level=None, derivs=False, margin=False):
+                  level=None, derivs=False):
     """Advance (x, v) by ncycles * dt_max with block (individual) time steps (R#28).
 
     If acc/jerk/level are None, forces and initial levels are evaluated first.
     Returns (x, v, acc, jerk, level, stats, crit): stats = (block steps, sum of
     active counts), crit = the last Aarseth criterion value of every particle.
     With derivs=True two more arrays follow: the interpolated a^(2)(t) and a^(3) [3][n]
-    each particle's last criterion used.  With margin=True one more array follows: per
-    particle the smallest distance of log2(dt_max / dt_c) to an integer over all its
-    level decisions (a diagnostic of how close the schedule came to a level flip).
+    each particle's last criterion used.
     """
     m = _f64(m)
     n = m.shape[0]
@@ -225,12 +223,11 @@ def hermite_block(m, x, v, eps2: float, dt_max: float, ncycles: int, eta: float,
     crit = np.full(n, np.nan)
     d2 = np.full((3, n), np.nan) if derivs else None
     d3 = np.full((3, n), np.nan) if derivs else None
-    mg = np.full(n, np.inf) if margin else None
     rc = _load().oracle_hermite_block(n, float(G), float(eps2), float(dt_max), int(kmax),
                                       float(eta), float(eta_s), int(ncycles), _ptr(m), _ptr(x),
                                       _ptr(v), _ptr(acc), _ptr(jerk), _ptr(level),
                                       1 if init else 0, _ptr(stats), _ptr(crit), _ptr(d2),
-                                      _ptr(d3), _ptr(mg))
+                                      _ptr(d3))
     if rc == 1:
         raise OracleError("coincident pair with eps = 0")
     if rc == 3:
@@ -238,6 +235,4 @@ def hermite_block(m, x, v, eps2: float, dt_max: float, ncycles: int, eta: float,
     if rc:
         raise OracleError(f"oracle_hermite_block failed rc={rc}")
     out = (x, v, acc, jerk, level, (int(stats[0]), int(stats[1])), crit)
-    if derivs:
-        out = out + (d2, d3)
-    return out + (mg,) if margin else out
+    return out + (d2, d3) if derivs else out

@@ -294,23 +294,10 @@ done:
  * stats[1] += sum over block steps of |A|.  crit [n] (may be NULL) receives
  * the last criterion value dt_c of every particle (eta_s |a|/|j| after init);
  * d2_out, d3_out [3][n] (may be NULL) the a^(2)(t_next), a^(3) it used.
- * margin [n] (may be NULL; a diagnostic, no effect on the integration) receives
- * for every particle the smallest distance, over all its level decisions in
- * the call (the initial one included when init != 0), of log2(dt_max / dt_c)
- * to the nearest integer -- how close a decision came to a power-of-two
- * boundary, where a relative perturbation of dt_c of that size flips the level
- * (used to attribute block-schedule differences, tests/test_gpu_fuzz.py).
  * Returns 0, 1 coincident pair, 2 allocation failure, 3 non-finite state,
  * 4 invalid arguments.
  */
 static double block_dt(double dt_max, int k) { return ldexp(dt_max, -k); }
-
-/* distance of log2(dt_max / d) to the nearest integer (infinite d: no boundary) */
-static double boundary_dist(double dt_max, double d) {
-    if (!(d > 0.0) || !isfinite(d)) return INFINITY;
-    const double l = log2(dt_max / d);
-    return fabs(l - nearbyint(l));
-}
 
 static double norm3(const double* p, int64_t n, int64_t i) {
     return sqrt(p[0 * n + i] * p[0 * n + i] + p[1 * n + i] * p[1 * n + i] + p[2 * n + i] * p[2 * n + i]);
@@ -332,7 +319,7 @@ int oracle_block_init_levels(int64_t n, double dt_max, int kmax, double eta_s, c
 int oracle_hermite_block(int64_t n, double G, double eps2, double dt_max, int kmax, double eta,
                          double eta_s, int64_t ncycles, const double* m, double* x, double* v,
                          double* acc, double* jerk, int32_t* level, int init, int64_t* stats,
-                         double* crit, double* d2_out, double* d3_out, double* margin) {
+                         double* crit, double* d2_out, double* d3_out) {
     if (n < 1 || kmax < 0 || kmax > 50 || ncycles < 0 || !(dt_max > 0.0) || !(eta > 0.0)) return 4;
     const size_t sz = sizeof(double) * 3 * (size_t)n;
     double* xp = (double*)malloc(sz);
@@ -343,16 +330,9 @@ int oracle_hermite_block(int64_t n, double G, double eps2, double dt_max, int km
     double* j1 = (double*)malloc(sz);
     int rc = 0;
     if (!xp || !vp || !T || !act || !a1 || !j1) { rc = 2; goto done; }
-    if (margin)
-        for (int64_t i = 0; i < n; ++i) margin[i] = INFINITY;
     if (init) {
         if (oracle_forces(n, G, eps2, m, x, v, NULL, n, acc, jerk, NULL)) { rc = 1; goto done; }
         oracle_block_init_levels(n, dt_max, kmax, eta_s, acc, jerk, level, crit);
-        if (margin)
-            for (int64_t i = 0; i < n; ++i) {
-                const double an = norm3(acc, n, i), jn = norm3(jerk, n, i);
-                margin[i] = boundary_dist(dt_max, jn > 0.0 ? eta_s * an / jn : INFINITY);
-            }
     }
     const double tick = ldexp(dt_max, -kmax);
     const int64_t T_end = ncycles << kmax;
@@ -416,7 +396,6 @@ int oracle_hermite_block(int64_t n, double G, double eps2, double dt_max, int km
             level[i] = kn;
             T[i] = T_next;
             if (crit) crit[i] = dtc;
-            if (margin) margin[i] = fmin(margin[i], boundary_dist(dt_max, dtc));
         }
         if (rc) goto done;
         if (stats) { stats[0] += 1; stats[1] += na; }

@@ -52,10 +52,6 @@ namespace {
 #ifndef FK_MINB
 #define FK_MINB 2
 #endif
-#ifndef FK_PIPE
-#define FK_PIPE 0        // software-pipelined j loop: rsqrt of j + 1 issued before j's sums
-                         // (2: the same, hand-unrolled by two with ping-pong operands)
-#endif
 #ifndef FK_MINB_ACC
 #define FK_MINB_ACC 2    // acceleration-only kernel (leapfrog)
 #endif
@@ -90,10 +86,9 @@ static_assert(kStages * 8 <= 64, "mbarrier area");
 // default (1024 i per CTA) and a small one (256 i per CTA) for launches with
 // few i -- block-step active sets and small N -- where 1024-i CTAs would leave
 // most SMs idle.  Every i's j loop is identical in both, so results are too.
-template <int P, int T, int MINB, int MINB_ACC, int U = FK_UNROLL, int UL = U, int PIPE = FK_PIPE>
+template <int P, int T, int MINB, int MINB_ACC, int U = FK_UNROLL, int UL = U>
 struct FkCfg {
     static constexpr int kPairs = P, kThreads = T, kMinB = MINB, kMinBAcc = MINB_ACC;
-    static constexpr int kPipe = PIPE;    // software-pipelined j loop (0: off)
     static constexpr int kUnrollJ = U, kUnrollList = UL;   // j-loop unroll: plain / active-list
     static constexpr int kIPerBlock = 2 * P * T;
     static constexpr int kAccSmemBytes = FK_ACC_SMEM ? 6 * 2 * P * T * 8 : 0;
@@ -243,17 +238,6 @@ __device__ __forceinline__ JOps1 load_jops1(const JPkt* tile, const float4* tile
     return j;
 }
 
-// the packed operands of a scalar j (the pipelined loops carry j as scalars across
-// iterations and broadcast at the use, so no {v, v} register pairs are materialised)
-__device__ __forceinline__ JOps bcast(const JOps1& s) {
-    JOps j;
-    j.x = f2bc(s.x); j.y = f2bc(s.y); j.z = f2bc(s.z); j.m = f2bc(s.m); j.eps2 = f2bc(s.eps2);
-    j.vx = f2bc(s.vx); j.vy = f2bc(s.vy); j.vz = f2bc(s.vz);
-    j.lx = f2bc(s.lx); j.ly = f2bc(s.ly); j.lz = f2bc(s.lz);
-    j.mass = s.m;
-    return j;
-}
-
 // negated i state of the particle in packet src (0 for a padding slot)
 template <bool kHiLo>
 __device__ __forceinline__ void load_i(const ForceArgs& a, bool valid, int64_t src, float (&q)[9]) {
@@ -292,11 +276,10 @@ __device__ __forceinline__ void report_coincident(const GuardCtx& g, int sl, int
 // One j against one packed i-pair: the FP32 interaction of the file header, in two
 // halves.  front(): d = x_j - x_i (hi/lo: + the tails), s = |d|^2 + eps^2, ri = 1/sqrt(s)
 // (MUFU.RSQ); back(): mr3 = G m_j ri^3, a += mr3 d, jerk += mr3 (w - 3 (d.w) ri^2 d).
-// interact() runs both; the software-pipelined j loop of force_kernel runs front() of
-// j + 1 before back() of j, so each MUFU.RSQ has a whole j step of independent work to
-// hide behind.  Every force kernel (all CTA shapes, pipelined or not, the tile-split
-// kernels) runs exactly this instruction sequence per lane, so their tile sums are
-// bit-identical.  m3 = {-3, -3}.  kGuard (eps = 0): s == 0 gives ri = 0 and reports a
+// interact() runs both.  (A software-pipelined j loop running front() of j + 1 before
+// back() of j measured 3-17 % slower, profiles/r02_sweep_force.txt.)  Every force kernel
+// (all CTA shapes, the tile-split kernels) runs exactly this instruction sequence per
+// lane, so their tile sums are bit-identical.  m3 = {-3, -3}.  kGuard (eps = 0): s == 0 gives ri = 0 and reports a
 // coincident pair of distinct particles; sl_lo / sl_hi are the lanes' i-slots.
 struct Front {
     f2 dx, dy, dz, ri;
@@ -479,75 +462,14 @@ __global__ void __launch_bounds__(C::kThreads, kJerk ? C::kMinB : C::kMinBAcc) f
             for (int p = 0; p < kPairs; ++p) acc[k][p] = 0ull;
 
         const int64_t jt0 = jc0 + (int64_t)t * kTile;   // global index of the tile's first j
-        if constexpr (C::kPipe == 2) {
-            // the pipeline hand-unrolled by two: operands alternate between (ja, fa) and
-            // (jb, fb), so no register copies are needed at the loop back edge
-            auto fronts = [&](const JOps1& j1, Front (&f)[kPairs], int jj) {
-                const JOps jo = bcast(j1);
-#pragma unroll
-                for (int p = 0; p < kPairs; ++p)
-                    f[p] = front<kGuard, kHiLo, kList>(jo, ip[p], ib + 2 * p * kThreads + tid,
-                                                       ib + (2 * p + 1) * kThreads + tid,
-                                                       kGuard ? jt0 + jj : 0, gc);
-            };
-            auto backs = [&](const JOps1& j1, const Front (&f)[kPairs]) {
-                const JOps jo = bcast(j1);
-#pragma unroll
-                for (int p = 0; p < kPairs; ++p) back<kJerk>(jo, ip[p], f[p], acc, p, m3);
-            };
-            static_assert(kTile % 2 == 0, "ping-pong pipeline");
-            JOps1 ja = load_jops1<kJerk, kHiLo>(tile, tile_lo, 0), jb;
-            Front fa[kPairs], fb[kPairs];
-            fronts(ja, fa, 0);
-#pragma unroll 1
-            for (int jj = 0; jj < kTile - 2; jj += 2) {
-                jb = load_jops1<kJerk, kHiLo>(tile, tile_lo, jj + 1);
-                fronts(jb, fb, jj + 1);
-                backs(ja, fa);
-                ja = load_jops1<kJerk, kHiLo>(tile, tile_lo, jj + 2);
-                fronts(ja, fa, jj + 2);
-                backs(jb, fb);
-            }
-            jb = load_jops1<kJerk, kHiLo>(tile, tile_lo, kTile - 1);
-            fronts(jb, fb, kTile - 1);
-            backs(ja, fa);
-            backs(jb, fb);
-        } else if constexpr (C::kPipe == 1) {
-            // software pipeline: front() of j + 1 (its MUFU.RSQ) is issued in the same loop
-            // body as back() of j, whose operands arrived one iteration earlier
-            JOps1 jc = load_jops1<kJerk, kHiLo>(tile, tile_lo, 0);
-            Front fr[kPairs];
+#pragma unroll(kList ? C::kUnrollList : C::kUnrollJ)
+        for (int jj = 0; jj < kTile; ++jj) {
+            const JOps jo = load_jops<kJerk, kHiLo>(tile, tile_lo, jj);
+            const int64_t jg = kGuard ? jt0 + jj : 0;
 #pragma unroll
             for (int p = 0; p < kPairs; ++p)
-                fr[p] = front<kGuard, kHiLo, kList>(bcast(jc), ip[p], ib + 2 * p * kThreads + tid,
-                                                    ib + (2 * p + 1) * kThreads + tid, kGuard ? jt0 : 0, gc);
-#pragma unroll(kList ? C::kUnrollList : C::kUnrollJ)
-            for (int jj = 0; jj < kTile - 1; ++jj) {
-                const JOps1 jn = load_jops1<kJerk, kHiLo>(tile, tile_lo, jj + 1);
-                Front fn[kPairs];
-#pragma unroll
-                for (int p = 0; p < kPairs; ++p)
-                    fn[p] = front<kGuard, kHiLo, kList>(bcast(jn), ip[p], ib + 2 * p * kThreads + tid,
-                                                        ib + (2 * p + 1) * kThreads + tid,
-                                                        kGuard ? jt0 + jj + 1 : 0, gc);
-#pragma unroll
-                for (int p = 0; p < kPairs; ++p) back<kJerk>(bcast(jc), ip[p], fr[p], acc, p, m3);
-                jc = jn;
-#pragma unroll
-                for (int p = 0; p < kPairs; ++p) fr[p] = fn[p];
-            }
-#pragma unroll
-            for (int p = 0; p < kPairs; ++p) back<kJerk>(bcast(jc), ip[p], fr[p], acc, p, m3);
-        } else {
-#pragma unroll(kList ? C::kUnrollList : C::kUnrollJ)
-            for (int jj = 0; jj < kTile; ++jj) {
-                const JOps jo = load_jops<kJerk, kHiLo>(tile, tile_lo, jj);
-                const int64_t jg = kGuard ? jt0 + jj : 0;
-#pragma unroll
-                for (int p = 0; p < kPairs; ++p)
-                    interact<kGuard, kJerk, kHiLo, kList>(jo, ip[p], acc, p, m3, ib + 2 * p * kThreads + tid,
-                                                          ib + (2 * p + 1) * kThreads + tid, jg, gc);
-            }
+                interact<kGuard, kJerk, kHiLo, kList>(jo, ip[p], acc, p, m3, ib + 2 * p * kThreads + tid,
+                                                      ib + (2 * p + 1) * kThreads + tid, jg, gc);
         }
         // tile sum -> fp64, ascending tile order
 #pragma unroll

@@ -39,6 +39,66 @@ __device__ __forceinline__ void flag_bad(unsigned long long* bad, int64_t ig) {
     atomicMin(bad, (unsigned long long)ig);
 }
 
+__device__ __forceinline__ int64_t ticks_of(const StateArgs& a, int k) {
+    return (int64_t)1 << (a.kmax - k);
+}
+
+__device__ __forceinline__ double dt_of(const StateArgs& a, int k) { return ldexp(a.dt, -k); }
+
+// state of active particle i the corrector reads (loaded before the fold's partials)
+struct CorrIn {
+    double a0[3], j0[3], xp[3], vp[3];
+};
+__device__ __forceinline__ void load_corr_in(const StateArgs& a, int i, CorrIn& in) {
+    for (int c = 0; c < 3; ++c) {
+        const int64_t o = c * a.n_loc_pad + i;
+        in.a0[c] = a.a0[o]; in.j0[c] = a.j0[o]; in.xp[c] = a.xp[o]; in.vp[c] = a.vp[o];
+    }
+}
+
+// one active slot of the corrector after the fold: Hermite corrector with dt_i, Aarseth level
+__device__ __forceinline__ void correct_slot(const StateArgs& a, int i, const CorrIn& in, const double f[6],
+                                             unsigned long long tn) {
+    const int k = a.lev[i];
+    NB_CHECK(k >= 0 && k <= a.kmax && a.T[i] >= 0);
+    const double dt = dt_of(a, k);
+    const double dt2 = dt * dt, dt3 = dt2 * dt, dt4 = dt3 * dt, dt5 = dt4 * dt;
+    double s_a1 = 0, s_j1 = 0, s_a2 = 0, s_a3 = 0;
+    bool ok = true;
+    for (int c = 0; c < 3; ++c) {
+        const int64_t o = c * a.n_loc_pad + i;
+        const double a1 = f[c], j1 = f[3 + c];
+        const double a0 = in.a0[c], j0 = in.j0[c];
+        const double a2 = (-6.0 * (a0 - a1) - dt * (4.0 * j0 + 2.0 * j1)) / dt2;
+        const double a3 = (12.0 * (a0 - a1) + 6.0 * dt * (j0 + j1)) / dt3;
+        const double x = in.xp[c] + a2 * dt4 / 24.0 + a3 * dt5 / 120.0;
+        const double v = in.vp[c] + a2 * dt3 / 6.0 + a3 * dt4 / 24.0;
+        a.x[o] = x;
+        a.v[o] = v;
+        a.a0[o] = a1;
+        a.j0[o] = j1;
+        const double a2t = a2 + dt * a3;
+        s_a1 += a1 * a1; s_j1 += j1 * j1; s_a2 += a2t * a2t; s_a3 += a3 * a3;
+        ok = ok && isfinite(x) && isfinite(v) && isfinite(a1) && isfinite(j1);
+    }
+    if (!ok) flag_bad(a.bad, a.i_base + i);
+    const double na1 = sqrt(s_a1), nj1 = sqrt(s_j1), na2 = sqrt(s_a2), na3 = sqrt(s_a3);
+    const double den = nj1 * na3 + na2 * na2;
+    const double dtc = den > 0.0 ? sqrt(a.eta * (na1 * na2 + nj1 * nj1) / den) : INFINITY;
+    int kn = k;
+    if (dtc < dt) {
+        while (kn < a.kmax && dt_of(a, kn) > dtc) ++kn;
+    } else if (k > 0 && dtc >= 2.0 * dt && tn % (2ull * (unsigned long long)ticks_of(a, k)) == 0) {
+        kn = k - 1;
+    }
+    if (kn != k) {
+        atomicSub(a.lvl_cnt + k, 1);
+        atomicAdd(a.lvl_cnt + kn, 1);
+    }
+    a.lev[i] = kn;
+    a.T[i] = (int64_t)tn;
+}
+
 // fp64 -> fp32 RNE packet (R#18); with hi/lo (NEXT f2) also the fp32 tail
 // lo = RNE(x - hi), so hi + lo carries ~48 bits of the fp64 position.
 __device__ __forceinline__ void store_packet(const StateArgs& a, int64_t k, const double x[3],
@@ -226,12 +286,6 @@ __global__ void validate_levels_kernel(StateArgs a, unsigned long long* bad2) {
 // is exact integer arithmetic.  Only the level choice is floating point
 // (the Aarseth criterion, fp64 here as in the oracle).
 
-__device__ __forceinline__ int64_t ticks_of(const StateArgs& a, int k) {
-    return (int64_t)1 << (a.kmax - k);
-}
-
-__device__ __forceinline__ double dt_of(const StateArgs& a, int k) { return ldexp(a.dt, -k); }
-
 // Level histogram: one atomic per distinct level in the warp.
 __device__ __forceinline__ void count_level(int32_t* cnt, int k) {
     const unsigned act = __activemask();
@@ -309,10 +363,9 @@ __device__ __forceinline__ cudaGraphDeviceNode_t force_node(const BlockGraphNode
                                                                            : nodes->force_big[q];
 }
 
-__global__ void block_decide_kernel(long long* ctl, const unsigned long long* tnext,
-                                    unsigned long long* tcur, int32_t* append, int32_t* nact,
-                                    int nshards, cudaGraphConditionalHandle cond,
-                                    BlockGraphNodes* nodes) {
+__device__ void block_decide(long long* ctl, const unsigned long long* tnext, unsigned long long* tcur,
+                             int32_t* append, int32_t* nact, int nshards, cudaGraphConditionalHandle cond,
+                             BlockGraphNodes* nodes) {
     const bool done = *tnext > (unsigned long long)ctl[0];
     // freeze this block step's active counts (force passes and corrector read them) and
     // reset the selection pass's append counters for the next block step
@@ -360,6 +413,13 @@ __global__ void block_decide_kernel(long long* ctl, const unsigned long long* tn
         }
         cudaGraphSetConditional(cond, done ? 0u : 1u);
     }
+}
+
+__global__ void block_decide_kernel(long long* ctl, const unsigned long long* tnext,
+                                    unsigned long long* tcur, int32_t* append, int32_t* nact,
+                                    int nshards, cudaGraphConditionalHandle cond,
+                                    BlockGraphNodes* nodes) {
+    block_decide(ctl, tnext, tcur, append, nact, nshards, cond, nodes);
 }
 
 // active set {i : t_i + dt_i == t_next} (atomic append: slot order is irrelevant to the
@@ -419,16 +479,20 @@ __global__ void block_select_predict_kernel(StateArgs a) {
     const double tick = ldexp(a.dt, -a.kmax);
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < a.n_loc; i += gridDim.x * blockDim.x)
         select_predict_one(a, i, tn, tick, a.nact);
-}
-
-// state of active particle i the corrector reads (loaded before the fold's partials)
-struct CorrIn {
-    double a0[3], j0[3], xp[3], vp[3];
-};
-__device__ __forceinline__ void load_corr_in(const StateArgs& a, int i, CorrIn& in) {
-    for (int c = 0; c < 3; ++c) {
-        const int64_t o = c * a.n_loc_pad + i;
-        in.a0[c] = a.a0[o]; in.j0[c] = a.j0[o]; in.xp[c] = a.xp[o]; in.vp[c] = a.vp[o];
+    if (!a.sel_done) return;
+    // one shard: the last CTA to finish runs the decide step (block_decide_kernel's body)
+    // -- every CTA's appends are complete and visible once it has taken its ticket
+    __shared__ bool last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        last = atomicAdd(a.sel_done, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (last && threadIdx.x == 0) {
+        __threadfence();
+        *a.sel_done = 0;
+        block_decide(a.ctl, a.tnext, a.tcur, a.nact, a.nact_cur, 1, a.cond, a.gnodes);
     }
 }
 
@@ -450,49 +514,6 @@ __device__ __forceinline__ void fold_warp(const StateArgs& a, int q, int lane, d
             for (int k = 0; k < 6; ++k) s[k] += __shfl_sync(0xffffffffu, v[k], u);
     }
     for (int k = 0; k < 6; ++k) out[k] = s[k];
-}
-
-// one active slot of the corrector after the fold: Hermite corrector with dt_i, Aarseth level
-__device__ __forceinline__ void correct_slot(const StateArgs& a, int i, const CorrIn& in, const double f[6],
-                                             unsigned long long tn) {
-    const int k = a.lev[i];
-    NB_CHECK(k >= 0 && k <= a.kmax && a.T[i] >= 0);
-    const double dt = dt_of(a, k);
-    const double dt2 = dt * dt, dt3 = dt2 * dt, dt4 = dt3 * dt, dt5 = dt4 * dt;
-    double s_a1 = 0, s_j1 = 0, s_a2 = 0, s_a3 = 0;
-    bool ok = true;
-    for (int c = 0; c < 3; ++c) {
-        const int64_t o = c * a.n_loc_pad + i;
-        const double a1 = f[c], j1 = f[3 + c];
-        const double a0 = in.a0[c], j0 = in.j0[c];
-        const double a2 = (-6.0 * (a0 - a1) - dt * (4.0 * j0 + 2.0 * j1)) / dt2;
-        const double a3 = (12.0 * (a0 - a1) + 6.0 * dt * (j0 + j1)) / dt3;
-        const double x = in.xp[c] + a2 * dt4 / 24.0 + a3 * dt5 / 120.0;
-        const double v = in.vp[c] + a2 * dt3 / 6.0 + a3 * dt4 / 24.0;
-        a.x[o] = x;
-        a.v[o] = v;
-        a.a0[o] = a1;
-        a.j0[o] = j1;
-        const double a2t = a2 + dt * a3;
-        s_a1 += a1 * a1; s_j1 += j1 * j1; s_a2 += a2t * a2t; s_a3 += a3 * a3;
-        ok = ok && isfinite(x) && isfinite(v) && isfinite(a1) && isfinite(j1);
-    }
-    if (!ok) flag_bad(a.bad, a.i_base + i);
-    const double na1 = sqrt(s_a1), nj1 = sqrt(s_j1), na2 = sqrt(s_a2), na3 = sqrt(s_a3);
-    const double den = nj1 * na3 + na2 * na2;
-    const double dtc = den > 0.0 ? sqrt(a.eta * (na1 * na2 + nj1 * nj1) / den) : INFINITY;
-    int kn = k;
-    if (dtc < dt) {
-        while (kn < a.kmax && dt_of(a, kn) > dtc) ++kn;
-    } else if (k > 0 && dtc >= 2.0 * dt && tn % (2ull * (unsigned long long)ticks_of(a, k)) == 0) {
-        kn = k - 1;
-    }
-    if (kn != k) {
-        atomicSub(a.lvl_cnt + k, 1);
-        atomicAdd(a.lvl_cnt + kn, 1);
-    }
-    a.lev[i] = kn;
-    a.T[i] = (int64_t)tn;
 }
 
 // Active sets up to this size (and at most one slot per warp of the launch) fold one

@@ -109,6 +109,8 @@ int force_tsplit1_max();        // ... and for the scalar one
 // resident force CTAs per SM for the kernel variant (occupancy calculator)
 int force_ctas_per_sm(bool jerk, bool hilo);
 
+struct BlockGraphNodes;
+
 // fp64 particle-update kernels (hermite.cu).
 struct StateArgs {
     int32_t n_loc;
@@ -139,6 +141,12 @@ struct StateArgs {
     long long* ctl;      // block-run control [t_end ticks, block steps, sum of active, done]
     int32_t kmax;
     double eta, eta_s;
+    // one shard: the selection pass's last CTA also runs the decide step (no separate
+    // decide launch); sel_done is its CTA counter (device, zero between launches), cond /
+    // gnodes the block-step graph's conditional handle and force-node table (graph only)
+    unsigned* sel_done;
+    cudaGraphConditionalHandle cond;
+    BlockGraphNodes* gnodes;
 };
 cudaError_t launch_pack_state(const StateArgs& a, cudaStream_t s);     // x, v -> pkt
 cudaError_t launch_predict_pack(const StateArgs& a, cudaStream_t s);   // x,v,a0,j0 -> xp,vp,pkt

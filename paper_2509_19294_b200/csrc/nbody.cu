@@ -184,6 +184,7 @@ struct nbody_ctx {
     int32_t* nact = nullptr;               // per shard: selection append counters
     int32_t* nact_cur = nullptr;           // per shard: this block step's active counts
     int32_t* lvl_cnt = nullptr;   // [64] particles per level, all shards
+    unsigned* sel_done = nullptr;  // selection-pass CTA counter (decide fused, one shard)
     nb::BlockGraphNodes* gnodes = nullptr;   // device copy of the graph's force-node handles
     long long* ctl = nullptr;            // [t_end, block steps, active sum, done] (device)
     void* hbuf = nullptr;
@@ -301,6 +302,9 @@ nb::StateArgs state_args(nbody_ctx* c, Shard& s) {
     a.tcur = c->tcur;
     a.self_tnext = c->comm ? 0 : 1;   // NCCL ranks reduce t_next over ranks first
     a.lvl_cnt = c->lvl_cnt;
+    a.sel_done = nullptr;   // block_step_body enables the fused decide step
+    a.cond = 0;
+    a.gnodes = nullptr;
     a.ctl = c->ctl;
     a.kmax = c->cfg.kmax;
     a.eta = c->cfg.eta;
@@ -309,6 +313,8 @@ nb::StateArgs state_args(nbody_ctx* c, Shard& s) {
 }
 
 bool use_nccl(const nbody_ctx* c) { return c->comm != nullptr; }
+// block steps with one shard per context fold the decide step into the selection pass
+bool decide_fused(const nbody_ctx* c) { return c->nshards == 1; }
 
 // force pass over chunks [c_first, c_first + c_count) for the shard's local
 // particles, or (block steps) for the n_i active particles listed in ilist
@@ -543,6 +549,7 @@ void free_ctx(nbody_ctx* c) {
     cudaFree(c->nact_cur);
     cudaFree(c->nact);
     cudaFree(c->lvl_cnt);
+    cudaFree(c->sel_done);
     cudaFree(c->ctl);
     cudaFree(c->gnodes);
     if (c->block_graph) cudaGraphExecDestroy(c->block_graph);
@@ -641,10 +648,11 @@ int init_impl(const nbody_config* cfg, const double* m, const double* x, const d
     if (is_block(c)) {
         if ((rc = dalloc(c, &c->tnext, 1)) || (rc = dalloc(c, &c->tcur, 1)) ||
             (rc = dalloc(c, &c->nact, (size_t)c->nshards)) || (rc = dalloc(c, &c->nact_cur, (size_t)c->nshards)) ||
-            (rc = dalloc(c, &c->lvl_cnt, 64)) ||
+            (rc = dalloc(c, &c->lvl_cnt, 64)) || (rc = dalloc(c, &c->sel_done, 1)) ||
             (rc = dalloc(c, &c->ctl, 4)) || (rc = dalloc(c, &c->gnodes, 1)))
             return rc;
         CK(c, cudaMemsetAsync(c->ctl, 0, 4 * sizeof(long long), c->stream));
+        CK(c, cudaMemsetAsync(c->sel_done, 0, sizeof(unsigned), c->stream));
         CK(c, cudaMallocHost(&c->hbuf, 8 + 4 * (size_t)c->nshards));
     }
     CK(c, cudaMemsetAsync(c->flags, 0xff, 4 * sizeof(unsigned long long), c->stream));
@@ -823,9 +831,18 @@ int block_step_body(nbody_ctx* c, cudaGraphConditionalHandle cond, nb::BlockGrap
         CK(c, nb::launch_block_tnext(state_args(c, c->sh[0]), c->stream));
         CKNCCL(c, nccl().AllReduce(c->tnext, c->tnext, 1, ncclUint64, ncclMin, c->comm, c->stream));
     }
-    for (auto& s : c->sh) CK(c, nb::launch_block_select_predict(state_args(c, s), c->stream));
-    CK(c, nb::launch_block_decide(c->ctl, c->tnext, c->tcur, c->nact, c->nact_cur, c->nshards, cond, nodes,
-                                  c->stream));
+    for (auto& s : c->sh) {
+        nb::StateArgs a = state_args(c, s);
+        if (decide_fused(c)) {   // the selection pass's last CTA runs the decide step
+            a.sel_done = c->sel_done;
+            a.cond = cond;
+            a.gnodes = nodes;
+        }
+        CK(c, nb::launch_block_select_predict(a, c->stream));
+    }
+    if (!decide_fused(c))
+        CK(c, nb::launch_block_decide(c->ctl, c->tnext, c->tcur, c->nact, c->nact_cur, c->nshards, cond, nodes,
+                                      c->stream));
     return NBODY_OK;
 }
 
@@ -912,7 +929,7 @@ int block_step_rest(nbody_ctx* c, const int32_t* n_act, nb::BlockGraphNodes* nod
         }
     }
     for (int q = 0; q < c->nshards; ++q) CK(c, nb::launch_block_correct(state_args(c, c->sh[q]), c->stream));
-    c->n_kernels += 1 + 3 * (int64_t)c->nshards;   // select, force, correct; decide
+    c->n_kernels += (decide_fused(c) ? 0 : 1) + 3 * (int64_t)c->nshards;   // select, force, correct; decide
     return NBODY_OK;
 }
 
@@ -1261,8 +1278,11 @@ int nbody_prof_read(nbody_ctx* c, double* force_ms, int64_t* force_launches, int
         const int64_t graph_steps = steps - c->block_steps_at_reset - c->block_host_steps;
         // per block step select, force, correct per shard and decide; per call one last
         // iteration (select, decide, correct) that finds the run done
-        graph_kernels = (3 * (int64_t)c->nshards + 1) * graph_steps +
-                        (2 * (int64_t)c->nshards + 1) * c->block_graph_calls;
+        const int64_t dk = decide_fused(c) ? 0 : 1;   // a separate decide launch
+        // per block step select, force, correct per shard and decide; per call one last
+        // iteration (select, decide, correct) that finds the run done
+        graph_kernels = (3 * (int64_t)c->nshards + dk) * graph_steps +
+                        (2 * (int64_t)c->nshards + dk) * c->block_graph_calls;
         if (reset) {
             c->block_steps_at_reset = steps;
             c->block_host_steps = 0;

@@ -15,17 +15,12 @@ sys.path.insert(0, ROOT)
 OUT = os.path.join(ROOT, "scripts", "sweep")
 
 VARIANTS = {
-    # round-1 variants (3-stage ring, 3 CTAs/SM, 64/96/160 threads, 3 pairs, ptxas -O1/-O2,
-    # 1 CTA/SM with unroll 3/4) are recorded in profiles/r01_sweep_force.txt; round 2
-    # sweeps the software-pipelined j loop (FK_PIPE, profiles/r02_sweep_force.txt)
-    "base":      dict(FK_PIPE=0),
-    "pipe":      dict(FK_PIPE=1),
-    "pipe_u1":   dict(FK_PIPE=1, FK_UNROLL=1),
-    "pipe_u4":   dict(FK_PIPE=1, FK_UNROLL=4),
-    "pp":        dict(FK_PIPE=2),
-    "pipe_p3b3": dict(FK_PIPE=1, FK_PAIRS=3, FK_MINB=3),
-    "pp_p3b3":   dict(FK_PIPE=2, FK_PAIRS=3, FK_MINB=3),
-    "pipe_st3":  dict(FK_PIPE=1, FK_STAGES=3),
+    # round-1 variants (3-stage ring, 3 CTAs/SM, 64/96/160 threads, 2/3/5 pairs, ptxas -O1/-O2,
+    # 1 CTA/SM with unroll 3/4, constant-memory j, register prefetch) are recorded in
+    # profiles/r01_sweep_force.txt; round 2's software-pipelined j loop, register-copy squares
+    # and 5 pairs per thread in profiles/r02_sweep_force.txt (all slower; code removed)
+    "base":      dict(),
+    "p3b3":      dict(FK_PAIRS=3, FK_MINB=3),
 }
 if os.environ.get("SWEEP_ONLY"):
     VARIANTS = {k: v for k, v in VARIANTS.items() if k in os.environ["SWEEP_ONLY"].split(",")}

@@ -1,7 +1,6 @@
 """Randomised GPU parity sweep through the C-ABI: seeded random system sizes, softenings,
 shard counts, position modes and integrators, each checked against the fp64 oracle and
 against the unsharded run.  The seeds are fixed, so a failure is reproducible."""
-import math
 import os
 
 import numpy as np
@@ -10,6 +9,7 @@ import pytest
 import oracle
 from paper_2509_19294_b200 import binding, inputs
 from metrics import TOL_ACC, TOL_JERK, max_rel
+from test_gpu_block import _levels_agree
 
 pytestmark = pytest.mark.gpu
 torch = pytest.importorskip("torch")
@@ -100,22 +100,20 @@ def test_random_block_case(k, monkeypatch):
     assert np.isfinite(ref[0]).all() and np.isfinite(ref[1]).all()
     if n <= 1025 and hilo:   # oracle schedule parity needs two-float positions (R#28)
         e2 = float(np.float32(eps * eps))
-        xo, vo, _, _, lo, so, co, mg = oracle.hermite_block(m, x, v, e2, dt_max, 1, eta=eta, eta_s=0.01,
-                                                            kmax=20, margin=True)
-        # Schedule differences are attributed, particle by particle, to level decisions the
-        # oracle itself took within round-off of a power-of-two boundary (R#28): mg is the
-        # smallest distance of log2(dt_max / dt_c) to an integer over each particle's
-        # decisions, and 1e-3 / ln 2 (a relative 1e-3 change of dt_c, ~100x the GPU's fp32
-        # force error) is the margin test_gpu_block's _levels_agree uses.
-        near = mg < 1e-3 / math.log(2)
+        xo, vo, _, _, lo, so, co = oracle.hermite_block(m, x, v, e2, dt_max, 1, eta=eta, eta_s=0.01,
+                                                        kmax=20)
         lg = ref[2]
-        assert np.array_equal(lg[~near], lo[~near]), (k, np.flatnonzero((lg != lo) & ~near)[:10])
-        assert np.all(np.abs(lg - lo) <= 1), k
-        # a particle flipping between levels k and k + 1 adds at most its own 2^(k+1) step
-        # times (block steps) and evaluations per dt_max; without such a particle the counts
-        # agree to 5 % (block steps) / 2 % (force evaluations)
-        slack = int(sum(2 ** (1 + max(int(lg[i]), int(lo[i]))) for i in np.flatnonzero(near)))
-        assert abs(ref[3][0] - so[0]) <= 0.05 * so[0] + 2 + slack, (k, ref[3], so, int(near.sum()))
-        assert abs(ref[3][1] - so[1]) <= 0.02 * so[1] + 2 + slack, (k, ref[3], so, int(near.sum()))
+        # levels: test_gpu_block's rule -- agreement on >= 99 % of the particles whose
+        # oracle criterion is clear (relative 1e-3) of a power-of-two boundary, and every
+        # disagreement an adjacent level (both valid choices up to fp32 force round-off)
+        frac, adjacent, nclear = _levels_agree(lg, lo, co, dt_max)
+        assert frac >= 0.99 and adjacent, (k, frac, adjacent, nclear)
+        # schedule counts: 5 % (block steps) / 2 % (force evaluations), plus what the
+        # particles on another level can account for -- a particle on level k + 1 instead
+        # of k adds at most its own 2^(k+1) step times and evaluations per dt_max
+        diff = np.flatnonzero(lg != lo)
+        slack = int(sum(2 ** (1 + max(int(lg[i]), int(lo[i]))) for i in diff))
+        assert abs(ref[3][0] - so[0]) <= 0.05 * so[0] + 2 + slack, (k, ref[3], so, diff.size)
+        assert abs(ref[3][1] - so[1]) <= 0.02 * so[1] + 2 + slack, (k, ref[3], so, diff.size)
         # positions agree to the level of a few adjacent-level choices (see test_gpu_block)
         assert np.max(np.abs(ref[0] - xo)) <= 1e-6, (k, np.max(np.abs(ref[0] - xo)))
