@@ -196,6 +196,7 @@ struct nbody_ctx {
     cudaEvent_t ev_packed = nullptr, ev_gathered = nullptr;
     ncclComm_t comm = nullptr;
     double nccl_timeout_s = 600.0;
+    bool loop_concurrent = false;   // loopback shards in the NCCL rank's stream form (NBODY_LOOPBACK_CONCURRENT)
     bool have_a0 = false, predicted = false;
     bool use_graph = true;
     cudaGraphExec_t step_graph = nullptr;
@@ -323,7 +324,9 @@ bool decide_fused(const nbody_ctx* c) { return c->nshards == 1; }
 // kForceBig (1024-i CTAs: the exchange-overlap launch, sized in whole waves of that shape)
 constexpr int kForceBig = 4;
 int launch_force_range(nbody_ctx* c, Shard& s, int32_t c_first, int32_t c_count, int32_t n_i = -1,
-                       const int32_t* ilist = nullptr, const int32_t* n_dev = nullptr, int tsplit = 0) {
+                       const int32_t* ilist = nullptr, const int32_t* n_dev = nullptr, int tsplit = 0,
+                       cudaStream_t st = nullptr) {
+    if (!st) st = c->stream;
     if (n_i < 0) n_i = s.n_loc;
     if (c_count <= 0 || n_i <= 0) return NBODY_OK;
     nb::ForceArgs f;
@@ -362,17 +365,17 @@ int launch_force_range(nbody_ctx* c, Shard& s, int32_t c_first, int32_t c_count,
         c->prof_nj.resize(c->prof_used / 2);
         c->prof_ni.back() = n_i;
         c->prof_nj.back() = nj;
-        CK(c, cudaEventRecord(e0, c->stream));
+        CK(c, cudaEventRecord(e0, st));
     }
     if (tsplit == 1 || tsplit == 2)
-        CK(c, nb::launch_force_tsplit(f, c->guard, ncomp(c) == 6, tsplit == 2, c->stream));
+        CK(c, nb::launch_force_tsplit(f, c->guard, ncomp(c) == 6, tsplit == 2, st));
     else if (ilist)
-        CK(c, nb::launch_force_list(f, c->guard, tsplit == 3, c->stream));
+        CK(c, nb::launch_force_list(f, c->guard, tsplit == 3, st));
     else if (tsplit == kForceBig)
-        CK(c, nb::launch_force_big(f, c->guard, ncomp(c) == 6, c->stream));
+        CK(c, nb::launch_force_big(f, c->guard, ncomp(c) == 6, st));
     else
-        CK(c, nb::launch_force(f, c->guard, ncomp(c) == 6, c->stream));
-    if (e1) CK(c, cudaEventRecord(e1, c->stream));
+        CK(c, nb::launch_force(f, c->guard, ncomp(c) == 6, st));
+    if (e1) CK(c, cudaEventRecord(e1, st));
     c->n_force++;
     c->n_kernels++;
     return NBODY_OK;
@@ -435,7 +438,12 @@ int32_t overlap_chunks(const nbody_ctx* c, const Shard& s) {
 }
 
 // exchange the packets every shard's pack kernel wrote and run every shard's force pass:
-// local chunks first (overlapping the exchange), the remaining chunks after it
+// local chunks first on the compute stream, overlapping the exchange on the comm stream;
+// the remaining chunks on the comm stream right behind the exchange, so that launch is
+// ordered after the data it reads but not after the local launch -- its CTAs take SM
+// slots as the local launch's CTAs drain instead of waiting for its last wave (two
+// stream-ordered launches would pay a partial wave each: C3 at P = 8 ran 8 waves of work
+// items for 6.9 waves of work); then the compute stream joins the comm stream.
 int exchange_and_force(nbody_ctx* c) {
     int rc;
     if (use_nccl(c)) {
@@ -443,13 +451,34 @@ int exchange_and_force(nbody_ctx* c) {
         CK(c, cudaEventRecord(c->ev_packed, c->stream));
         CK(c, cudaStreamWaitEvent(c->comm_stream, c->ev_packed, 0));
         if ((rc = gather_packets(c, c->comm_stream))) return rc;
-        CK(c, cudaEventRecord(c->ev_gathered, c->comm_stream));
         const int32_t f = overlap_chunks(c, s), nch = (int32_t)s.plan.n_chunks;
         if ((rc = launch_force_range(c, s, s.c_lo, f, -1, nullptr, nullptr, kForceBig))) return rc;
+        if ((rc = launch_force_range(c, s, (s.c_lo + f) % nch, nch - f, -1, nullptr, nullptr, 0, c->comm_stream)))
+            return rc;
+        CK(c, cudaEventRecord(c->ev_gathered, c->comm_stream));
         CK(c, cudaStreamWaitEvent(c->stream, c->ev_gathered, 0));
-        if ((rc = launch_force_range(c, s, (s.c_lo + f) % nch, nch - f))) return rc;
+    } else if (c->nshards > 1 && c->loop_concurrent) {
+        // loopback, timing form (scripts/project_scaling.py): per shard the rank's streams --
+        // the emulated gather (one copy per slice) and the remote launch on the comm stream,
+        // concurrent with the local-first launch; shards joined one after another
+        for (int q = 0; q < c->nshards; ++q) {
+            Shard& s = c->sh[q];
+            const int32_t f = overlap_chunks(c, s), nch = (int32_t)s.plan.n_chunks;
+            CK(c, cudaEventRecord(c->ev_packed, c->stream));
+            CK(c, cudaStreamWaitEvent(c->comm_stream, c->ev_packed, 0));
+            if ((rc = gather_into(c, q, c->comm_stream))) return rc;
+            if ((rc = launch_force_range(c, s, s.c_lo, f, -1, nullptr, nullptr, kForceBig))) return rc;
+            if ((rc = launch_force_range(c, s, (s.c_lo + f) % nch, nch - f, -1, nullptr, nullptr, 0,
+                                         c->comm_stream)))
+                return rc;
+            CK(c, cudaEventRecord(c->ev_gathered, c->comm_stream));
+            CK(c, cudaStreamWaitEvent(c->stream, c->ev_gathered, 0));
+        }
     } else if (c->nshards > 1) {
-        // loopback: per shard the same two launches, the emulated gather between them
+        // loopback, checking form (default): per shard the same two launches with the emulated
+        // gather strictly between them on one stream, so a local-first launch that reads a
+        // remote chunk always reads the previous step's data and a wrong slice offset always
+        // lands in the remote launch's input (tests/test_gpu_exchange.py)
         for (int q = 0; q < c->nshards; ++q) {
             Shard& s = c->sh[q];
             const int32_t f = overlap_chunks(c, s), nch = (int32_t)s.plan.n_chunks;
@@ -608,6 +637,7 @@ int init_impl(const nbody_config* cfg, const double* m, const double* x, const d
     c->eps2f = (float)(k.eps * k.eps);
     c->guard = c->eps2f < FLT_MIN;   // 0, or subnormal (flushed to 0 by the FTZ force pass)
     if (const char* t = getenv("NBODY_NCCL_TIMEOUT_S"); t && *t && atof(t) > 0) c->nccl_timeout_s = atof(t);
+    if (const char* t = getenv("NBODY_LOOPBACK_CONCURRENT"); t && *t && *t != '0') c->loop_concurrent = true;
     c->nshards = k.loopback ? k.world : 1;
     c->sh.resize(c->nshards);
     std::string why;

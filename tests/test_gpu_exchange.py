@@ -91,11 +91,16 @@ def test_nccl_step_path_graph_and_eager(cfg, nsteps):
     assert np.linalg.norm(ref[3] - vo, axis=0).max() <= dv_tol
 
 
+@pytest.mark.parametrize("concurrent", ["0", "1"])
 @pytest.mark.parametrize("world", [2, 3, 8])
-def test_loopback_exchange_graph_and_eager(world):
+def test_loopback_exchange_graph_and_eager(world, concurrent, monkeypatch):
     """Loopback shards with their own exchange buffers and per-slice copies equal the
     single-shard run bit for bit (graph replay and eager), with per shard one local-first
-    launch over chunks inside its own slice and one launch over the rest."""
+    launch over chunks inside its own slice and one launch over the rest -- in the checking
+    form (copies between the launches on one stream) and in the NCCL rank's stream form
+    (copies and remote launch on the comm stream, concurrent with the local launch;
+    NBODY_LOOPBACK_CONCURRENT=1, the form scripts/project_scaling.py times)."""
+    monkeypatch.setenv("NBODY_LOOPBACK_CONCURRENT", concurrent)
     n = 20000 if world != 8 else 16384 + 1000   # ragged: the last shard is short or empty
     m, x, v = inputs.parity_round(*inputs.plummer(n, 31 + world))
     st = torch.cuda.Stream()
