@@ -51,6 +51,9 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=10.0)
     p.add_argument("--no-flush", action="store_true")
+    p.add_argument("--nccl1", action="store_true",
+                   help="with one GPU: run the multi-rank code path through a 1-rank NCCL communicator "
+                        "(all-gather on the comm stream, local-first + concurrent remote force launches)")
     return p.parse_args()
 
 
@@ -280,6 +283,8 @@ def main():
         obj = [binding.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         nccl_id = obj[0]
+    elif args.nccl1:
+        nccl_id = binding.nccl_unique_id()
 
     block = args.integrator == "block"
     hilo = args.hilo == "on" or (args.hilo == "auto" and block)
@@ -449,6 +454,8 @@ def main():
                 "l2": "flushed between steps (256 MiB memset outside the per-step events)"
                       if flush is not None else "not flushed",
                 "parallelism": f"i-shard x{world}",
+                "exchange": ("ncclAllGather (1-rank communicator, --nccl1)" if world == 1 and args.nccl1
+                             else "ncclAllGather" if world > 1 else "none (one GPU holds every packet)"),
                 "j_split": {k: plan_info[k] for k in ("chunk", "n_chunks")} | {
                     "i_per_cta": 1024, "work_items_per_gpu": plan_info["items"],
                     "note": "canonical (i-block x j-chunk) work items; results bit-identical for any P"},
