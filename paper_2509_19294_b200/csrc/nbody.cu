@@ -27,6 +27,7 @@
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX v3: ranges cost nothing unless a tool is attached
 
 #include <sched.h>
 
@@ -49,6 +50,15 @@ using nb::JPkt;
 namespace {
 
 thread_local std::string g_last_error = "";
+
+// NVTX range for profilers (nsys / ncu --nvtx): every C-ABI entry point and, on the eager
+// path, every phase of a step is a named range (inside a CUDA graph only its launch is)
+struct Nvtx {
+    explicit Nvtx(const char* name) { nvtxRangePushA(name); }
+    ~Nvtx() { nvtxRangePop(); }
+    Nvtx(const Nvtx&) = delete;
+    Nvtx& operator=(const Nvtx&) = delete;
+};
 
 // ------------------------------------------------------------------ NCCL
 
@@ -445,6 +455,7 @@ int32_t overlap_chunks(const nbody_ctx* c, const Shard& s) {
 // stream-ordered launches would pay a partial wave each: C3 at P = 8 ran 8 waves of work
 // items for 6.9 waves of work); then the compute stream joins the comm stream.
 int exchange_and_force(nbody_ctx* c) {
+    Nvtx r("nbody: exchange + force");
     int rc;
     if (use_nccl(c)) {
         Shard& s = c->sh[0];
@@ -784,6 +795,7 @@ int nbody_nccl_unique_id(uint8_t out[128]) {
 
 int nbody_init(const nbody_config* cfg, const double* m, const double* x, const double* v,
                nbody_ctx** out) {
+    Nvtx r("nbody_init");
     if (!out) return fail(nullptr, NBODY_EINVAL, "out is NULL");
     *out = nullptr;
     if (!cfg) return fail(nullptr, NBODY_EINVAL, "cfg is NULL");
@@ -806,6 +818,7 @@ int nbody_local_range(const nbody_ctx* c, int64_t* i0, int64_t* i1) {
 }
 
 int nbody_compute_forces(nbody_ctx* c, double* acc, double* jerk) {
+    Nvtx r("nbody_compute_forces");
     GUARD(c);
     int rc;
     c->have_a0 = false;
@@ -835,6 +848,7 @@ namespace {
 int one_step(nbody_ctx* c) {
     int rc;
     if ((rc = exchange_and_force(c))) return rc;
+    Nvtx r("nbody: fold + correct + predict + pack");
     for (auto& s : c->sh) {
         CK(c, nb::launch_correct_predict_pack(state_args(c, s), c->stream));
         c->n_kernels++;
@@ -1066,6 +1080,7 @@ int block_run_host(nbody_ctx* c) {
 }  // namespace
 
 int nbody_step(nbody_ctx* c, int32_t nsteps) {
+    Nvtx r("nbody_step");
     GUARD(c);
     if (nsteps < 1) return fail(c, NBODY_EINVAL, "nsteps must be >= 1");
     int rc;
@@ -1113,6 +1128,7 @@ int nbody_step(nbody_ctx* c, int32_t nsteps) {
 }
 
 int nbody_energy(nbody_ctx* c, double* kinetic, double* potential) {
+    Nvtx r("nbody_energy");
     GUARD(c);
     int rc;
     if (!c->eall) {
@@ -1365,6 +1381,9 @@ const char* nbody_last_error(const nbody_ctx* c) {
     return g_last_error.c_str();
 }
 
-void nbody_destroy(nbody_ctx* c) { free_ctx(c); }
+void nbody_destroy(nbody_ctx* c) {
+    Nvtx r("nbody_destroy");
+    free_ctx(c);
+}
 
 }  // extern "C"
