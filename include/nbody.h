@@ -89,7 +89,11 @@ typedef struct {
                              buffer; the all-gather is emulated by one device
                              copy per remote slice into it, issued between the
                              same local-chunk and remote-chunk force launches
-                             an NCCL rank issues.  Outputs cover all n.        */
+                             an NCCL rank issues (environment
+                             NBODY_LOOPBACK_CONCURRENT=1: in the rank's stream
+                             form instead -- copies and remote launch on a
+                             second stream, concurrent with the local launch).
+                             Outputs cover all n.                              */
     int32_t jchunks;      /* max number of j-chunks of the canonical reduction
                              (0 -> 128).  Must be equal on every rank.          */
     int32_t hilo;         /* != 0: two-float positions (NEXT f2): packets also
