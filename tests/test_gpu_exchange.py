@@ -91,6 +91,20 @@ def test_nccl_step_path_graph_and_eager(cfg, nsteps):
     assert np.linalg.norm(ref[3] - vo, axis=0).max() <= dv_tol
 
 
+@pytest.mark.parametrize("integrator,hilo,eps", [("leapfrog", False, 1e-3), ("hermite", True, 1e-3),
+                                                 ("hermite", False, 0.0)])
+def test_nccl_step_path_other_modes(integrator, hilo, eps):
+    """The rank code path (1-rank NCCL communicator, graph-captured, two concurrent force
+    launches) for the acceleration-only leapfrog kernel, hi/lo position tails (a second
+    all-gather) and the eps = 0 guarded kernel: bit-identical to the communicator-free run."""
+    m, x, v = inputs.parity_round(*inputs.plummer(20000, 57))
+    st = torch.cuda.Stream()
+    kw = dict(integrator=integrator, hilo=hilo)
+    ref, _, _ = run(m, x, v, eps, 1 / 1024, 5, stream=st, **kw)
+    got, (g, e), _ = run(m, x, v, eps, 1 / 1024, 5, stream=st, nccl_id=binding.nccl_unique_id(), **kw)
+    assert g == 5 and e == 0 and same(got, ref)
+
+
 @pytest.mark.parametrize("concurrent", ["0", "1"])
 @pytest.mark.parametrize("world", [2, 3, 8])
 def test_loopback_exchange_graph_and_eager(world, concurrent, monkeypatch):
