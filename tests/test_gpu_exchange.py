@@ -254,3 +254,11 @@ def test_softening_outside_fp32_range_is_rejected():
     with pytest.raises(binding.NBodyError, match="fp32 range") as e:
         binding.NBody(m, x, v, eps=1e-13, dt=1 / 1024)
     assert e.value.code == binding.NBODY_EINVAL
+
+
+def test_multi_gpu_example_runs():
+    """examples/multi_gpu.py (the user-facing multi-rank recipe) with 3 emulated ranks."""
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "examples", "multi_gpu.py"), "C1", "5",
+                        "--loopback", "3"], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert "ranks = 3" in r.stdout and "relative drift" in r.stdout, r.stdout
