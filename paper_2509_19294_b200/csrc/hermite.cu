@@ -616,8 +616,10 @@ cudaError_t launch_block_reset_time(const StateArgs& a, cudaStream_t s) {
     return cudaGetLastError();
 }
 cudaError_t launch_block_select_predict(const StateArgs& a, cudaStream_t s) {
-    if (a.n_loc <= 0) return cudaSuccess;
-    block_select_predict_kernel<<<dims_for(a.n_loc).grid, dims_for(a.n_loc).block, 0, s>>>(a);
+    // a rank that owns no particles still runs the fused decide step (one CTA, no particles)
+    if (a.n_loc <= 0 && !a.sel_done) return cudaSuccess;
+    const Dims d = dims_for(a.n_loc > 0 ? a.n_loc : 1);
+    block_select_predict_kernel<<<d.grid, d.block, 0, s>>>(a);
     return cudaGetLastError();
 }
 cudaError_t launch_block_correct(const StateArgs& a, cudaStream_t s) {
