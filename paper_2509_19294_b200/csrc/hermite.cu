@@ -497,23 +497,37 @@ __global__ void block_select_predict_kernel(StateArgs a) {
 }
 
 // fold of slot q's chunk partials by one warp: lane l loads chunk c0 + l of every
-// component (32 chunks in flight per load round instead of one thread's serial walk),
-// then every lane adds the 32 values in ascending chunk order from shuffles -- the same
-// additions, in the same order, as fold_all
-__device__ __forceinline__ void fold_warp(const StateArgs& a, int q, int lane, double out[6]) {
+// component (32 chunks in flight per load round instead of one thread's serial walk) --
+// the same additions, in the same order, as fold_all.  The 32 values of a round go through
+// the warp's shared-memory slab red[32][6]: lane k < 6
+// then adds component k's 32 values in ascending chunk order (6 active lanes, 32 LDS + 32
+// DADD each, instead of 192 64-bit shuffles + 192 DADD in every lane), and the next
+// round's loads are issued before this round's adds (C2 block steps 5.00 -> 4.68 ms per
+// dt_max, C3 76.0 -> 74.1, interleaved A/B against the shuffle form, profiles/r02_fold_ab.jsonl).
+__device__ __forceinline__ void fold_warp(const StateArgs& a, int q, int lane, double out[6],
+                                          double (*red)[6]) {
     const double* p = a.partial + q;
     const int64_t row = a.n_loc_pad, stride = (int64_t)a.ncomp * a.n_loc_pad;
-    double s[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-    for (int c0 = 0; c0 < a.n_chunks; c0 += 32) {
-        const int c = c0 + lane, cnt = min(32, a.n_chunks - c0);
-        double v[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-        if (c < a.n_chunks)
-            for (int k = 0; k < 6; ++k) v[k] = p[c * stride + k * row];
-        for (int u = 0; u < cnt; ++u)
+    double s = 0.0;   // lane k < 6: component k
+    double v[6];
+    auto load = [&](int c0) {
+        const int c = c0 + lane;
 #pragma unroll
-            for (int k = 0; k < 6; ++k) s[k] += __shfl_sync(0xffffffffu, v[k], u);
+        for (int k = 0; k < 6; ++k) v[k] = c < a.n_chunks ? p[c * stride + k * row] : 0.0;
+    };
+    load(0);
+    for (int c0 = 0; c0 < a.n_chunks; c0 += 32) {
+        const int cnt = min(32, a.n_chunks - c0);
+#pragma unroll
+        for (int k = 0; k < 6; ++k) red[lane][k] = v[k];
+        __syncwarp();
+        if (c0 + 32 < a.n_chunks) load(c0 + 32);   // next round in flight during the adds
+        if (lane < 6)
+            for (int u = 0; u < cnt; ++u) s += red[u][lane];
+        __syncwarp();
     }
-    for (int k = 0; k < 6; ++k) out[k] = s[k];
+#pragma unroll
+    for (int k = 0; k < 6; ++k) out[k] = __shfl_sync(0xffffffffu, s, k);
 }
 
 // Active sets up to this size (and at most one slot per warp of the launch) fold one
@@ -526,6 +540,7 @@ __global__ void block_correct_kernel(StateArgs a) {
     const unsigned long long tn = *a.tnext;
     const int nw = (int)((gridDim.x * blockDim.x) >> 5);
     if (n_act <= min(kWarpFoldMax, nw) && a.ncomp == 6) {   // at most one slot per warp
+        __shared__ double red[kBlock / 32][32][6];   // one fold slab per warp
         const int lane = threadIdx.x & 31;
         for (int q = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5); q < n_act; q += nw) {
             const int i = a.ilist[q];
@@ -533,7 +548,7 @@ __global__ void block_correct_kernel(StateArgs a) {
             CorrIn in;
             if (lane == 0) load_corr_in(a, i, in);
             double f[6];
-            fold_warp(a, q, lane, f);
+            fold_warp(a, q, lane, f, red[threadIdx.x >> 5]);
             if (lane == 0) correct_slot(a, i, in, f, tn);
         }
     } else {
