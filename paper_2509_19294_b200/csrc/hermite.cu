@@ -56,33 +56,34 @@ __device__ __forceinline__ void load_corr_in(const StateArgs& a, int i, CorrIn& 
     }
 }
 
-// one active slot of the corrector after the fold: Hermite corrector with dt_i, Aarseth level
-__device__ __forceinline__ void correct_slot(const StateArgs& a, int i, const CorrIn& in, const double f[6],
-                                             unsigned long long tn) {
-    const int k = a.lev[i];
-    NB_CHECK(k >= 0 && k <= a.kmax && a.T[i] >= 0);
-    const double dt = dt_of(a, k);
+// One component c of the block corrector for active particle i after the fold: Hermite
+// corrector with dt_i (R#3), a0 <- a1, j0 <- j1; returns the four squares the Aarseth
+// criterion sums.  Products and sums of the criterion are explicitly rounded (no FMA
+// contraction), so the serial form (correct_slot) and the warp form (one lane per
+// component, block_correct_kernel) give the same bits.
+__device__ __forceinline__ bool correct_comp(const StateArgs& a, int i, int c, double dt, double a0, double j0,
+                                             double xp, double vp, double a1, double j1, double sq[4]) {
     const double dt2 = dt * dt, dt3 = dt2 * dt, dt4 = dt3 * dt, dt5 = dt4 * dt;
-    double s_a1 = 0, s_j1 = 0, s_a2 = 0, s_a3 = 0;
-    bool ok = true;
-    for (int c = 0; c < 3; ++c) {
-        const int64_t o = c * a.n_loc_pad + i;
-        const double a1 = f[c], j1 = f[3 + c];
-        const double a0 = in.a0[c], j0 = in.j0[c];
-        const double a2 = (-6.0 * (a0 - a1) - dt * (4.0 * j0 + 2.0 * j1)) / dt2;
-        const double a3 = (12.0 * (a0 - a1) + 6.0 * dt * (j0 + j1)) / dt3;
-        const double x = in.xp[c] + a2 * dt4 / 24.0 + a3 * dt5 / 120.0;
-        const double v = in.vp[c] + a2 * dt3 / 6.0 + a3 * dt4 / 24.0;
-        a.x[o] = x;
-        a.v[o] = v;
-        a.a0[o] = a1;
-        a.j0[o] = j1;
-        const double a2t = a2 + dt * a3;
-        s_a1 += a1 * a1; s_j1 += j1 * j1; s_a2 += a2t * a2t; s_a3 += a3 * a3;
-        ok = ok && isfinite(x) && isfinite(v) && isfinite(a1) && isfinite(j1);
-    }
+    const int64_t o = c * a.n_loc_pad + i;
+    const double a2 = (-6.0 * (a0 - a1) - dt * (4.0 * j0 + 2.0 * j1)) / dt2;
+    const double a3 = (12.0 * (a0 - a1) + 6.0 * dt * (j0 + j1)) / dt3;
+    const double x = xp + a2 * dt4 / 24.0 + a3 * dt5 / 120.0;
+    const double v = vp + a2 * dt3 / 6.0 + a3 * dt4 / 24.0;
+    a.x[o] = x;
+    a.v[o] = v;
+    a.a0[o] = a1;
+    a.j0[o] = j1;
+    const double a2t = a2 + dt * a3;   // a^(2) at t_next
+    sq[0] = __dmul_rn(a1, a1); sq[1] = __dmul_rn(j1, j1);
+    sq[2] = __dmul_rn(a2t, a2t); sq[3] = __dmul_rn(a3, a3);
+    return isfinite(x) && isfinite(v) && isfinite(a1) && isfinite(j1);
+}
+
+// the Aarseth criterion from the summed squares and the new level (R#28)
+__device__ __forceinline__ void correct_finish(const StateArgs& a, int i, int k, double dt, const double s[4],
+                                               bool ok, unsigned long long tn) {
     if (!ok) flag_bad(a.bad, a.i_base + i);
-    const double na1 = sqrt(s_a1), nj1 = sqrt(s_j1), na2 = sqrt(s_a2), na3 = sqrt(s_a3);
+    const double na1 = sqrt(s[0]), nj1 = sqrt(s[1]), na2 = sqrt(s[2]), na3 = sqrt(s[3]);
     const double den = nj1 * na3 + na2 * na2;
     const double dtc = den > 0.0 ? sqrt(a.eta * (na1 * na2 + nj1 * nj1) / den) : INFINITY;
     int kn = k;
@@ -97,6 +98,22 @@ __device__ __forceinline__ void correct_slot(const StateArgs& a, int i, const Co
     }
     a.lev[i] = kn;
     a.T[i] = (int64_t)tn;
+}
+
+// one active slot of the corrector after the fold, serially over the components
+__device__ __forceinline__ void correct_slot(const StateArgs& a, int i, const CorrIn& in, const double f[6],
+                                             unsigned long long tn) {
+    const int k = a.lev[i];
+    NB_CHECK(k >= 0 && k <= a.kmax && a.T[i] >= 0);
+    const double dt = dt_of(a, k);
+    double s[4] = {0.0, 0.0, 0.0, 0.0};
+    bool ok = true;
+    for (int c = 0; c < 3; ++c) {
+        double sq[4];
+        ok = correct_comp(a, i, c, dt, in.a0[c], in.j0[c], in.xp[c], in.vp[c], f[c], f[3 + c], sq) && ok;
+        for (int q = 0; q < 4; ++q) s[q] = __dadd_rn(s[q], sq[q]);
+    }
+    correct_finish(a, i, k, dt, s, ok, tn);
 }
 
 // fp64 -> fp32 RNE packet (R#18); with hi/lo (NEXT f2) also the fp32 tail
@@ -545,11 +562,28 @@ __global__ void block_correct_kernel(StateArgs a) {
         for (int q = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5); q < n_act; q += nw) {
             const int i = a.ilist[q];
             NB_CHECK(q < a.n_loc && i >= 0 && i < a.n_loc);
-            CorrIn in;
-            if (lane == 0) load_corr_in(a, i, in);
+            // lanes 0..2 load their component's state first (before the fold's loads)
+            const int cc = lane < 3 ? lane : 0;
+            const int64_t o = cc * a.n_loc_pad + i;
+            const double a0 = a.a0[o], j0 = a.j0[o], xp = a.xp[o], vp = a.vp[o];
+            const int k = a.lev[i];
             double f[6];
             fold_warp(a, q, lane, f, red[threadIdx.x >> 5]);
-            if (lane == 0) correct_slot(a, i, in, f, tn);
+            // corrector: one lane per component, lane 0 sums the criterion's squares in
+            // component order and sets the level (the arithmetic of correct_slot)
+            const double dt = dt_of(a, k);
+            double sq[4] = {0.0, 0.0, 0.0, 0.0};
+            bool ok = true;
+            if (lane < 3) ok = correct_comp(a, i, lane, dt, a0, j0, xp, vp, f[lane], f[3 + lane], sq);
+            const bool all_ok = __all_sync(0xffffffffu, ok);
+            double s4[4] = {0.0, 0.0, 0.0, 0.0};
+            for (int c = 0; c < 3; ++c)
+#pragma unroll
+                for (int r = 0; r < 4; ++r) s4[r] = __dadd_rn(s4[r], __shfl_sync(0xffffffffu, sq[r], c));
+            if (lane == 0) {
+                NB_CHECK(k >= 0 && k <= a.kmax && a.T[i] >= 0);
+                correct_finish(a, i, k, dt, s4, all_ok, tn);
+            }
         }
     } else {
         for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n_act; q += gridDim.x * blockDim.x) {
