@@ -444,23 +444,35 @@ __global__ void block_decide_kernel(long long* ctl, const unsigned long long* tn
 // its own polynomial (the predictor of predict() with dt -> D = t_next - t_i), packed for
 // the exchange.  In the block step past t_end the prediction is scratch nobody reads.
 // one particle of the active-set selection + prediction pass (append to *nact / ilist)
-__device__ __forceinline__ void select_predict_one(const StateArgs& a, int i, unsigned long long tn,
-                                                   double tick, int32_t* nact) {
-    NB_CHECK((unsigned long long)(a.T[i] + ticks_of(a, a.lev[i])) >= tn);   // none left behind
-    const bool active = (unsigned long long)(a.T[i] + ticks_of(a, a.lev[i])) == tn;
+// the state one particle's selection + prediction reads, loaded ahead of t_next
+struct SelIn {
+    double x[3], v[3], ac[3], jk[3], m;
+    int64_t T;
+    int32_t lev;
+};
+__device__ __forceinline__ void load_sel_in(const StateArgs& a, int i, SelIn& in) {
+    for (int c = 0; c < 3; ++c) {
+        const int64_t o = c * a.n_loc_pad + i;
+        in.x[c] = a.x[o]; in.v[c] = a.v[o]; in.ac[c] = a.a0[o]; in.jk[c] = a.j0[o];
+    }
+    in.m = a.m[i];
+    in.T = a.T[i];
+    in.lev = a.lev[i];
+}
+__device__ __forceinline__ void select_predict_one(const StateArgs& a, int i, const SelIn& in,
+                                                   unsigned long long tn, double tick, int32_t* nact) {
+    NB_CHECK((unsigned long long)(in.T + ticks_of(a, in.lev)) >= tn);   // none left behind
+    const bool active = (unsigned long long)(in.T + ticks_of(a, in.lev)) == tn;
     if (active) {
         const int slot = atomicAdd(nact, 1);
         NB_CHECK(slot >= 0 && slot < a.n_loc);
         a.ilist[slot] = i;
     }
-    const double D = (double)(int64_t)(tn - (unsigned long long)a.T[i]) * tick;
+    const double D = (double)(int64_t)(tn - (unsigned long long)in.T) * tick;
     const double D2 = D * D, D3 = D2 * D;
-    double xp[3], vp[3], xs[3], vs[3], as[3], js[3];
+    double xp[3], vp[3];
+    const double *xs = in.x, *vs = in.v, *as = in.ac, *js = in.jk;
     bool ok = true;
-    for (int c = 0; c < 3; ++c) {   // loads first (see correct_predict_pack_kernel)
-        const int64_t o = c * a.n_loc_pad + i;
-        xs[c] = a.x[o]; vs[c] = a.v[o]; as[c] = a.a0[o]; js[c] = a.j0[o];
-    }
     for (int c = 0; c < 3; ++c) {
         const int64_t o = c * a.n_loc_pad + i;
         const double x = xs[c], v = vs[c], ac = as[c], jk = js[c];
@@ -473,10 +485,14 @@ __device__ __forceinline__ void select_predict_one(const StateArgs& a, int i, un
         ok = ok && isfinite(xp[c]) && isfinite(vp[c]);
     }
     if (!ok) flag_bad(a.bad, a.i_base + i);
-    store_packet(a, a.i_base + i, xp, vp, a.G * a.m[i]);
+    store_packet(a, a.i_base + i, xp, vp, a.G * in.m);
 }
 
 __global__ void block_select_predict_kernel(StateArgs a) {
+    // the first particle's state is loaded before t_next (its L2 round trip overlaps them)
+    const int i_first = blockIdx.x * blockDim.x + threadIdx.x;
+    SelIn first;
+    if (i_first < a.n_loc) load_sel_in(a, i_first, first);
     // t_next: from the level counts the previous corrector left (every CTA derives the same
     // value; CTA 0 publishes it for decide / force / corrector), or given (NCCL ranks)
     __shared__ unsigned long long tn_s;
@@ -494,8 +510,12 @@ __global__ void block_select_predict_kernel(StateArgs a) {
     __syncthreads();
     const unsigned long long tn = tn_s;
     const double tick = ldexp(a.dt, -a.kmax);
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < a.n_loc; i += gridDim.x * blockDim.x)
-        select_predict_one(a, i, tn, tick, a.nact);
+    if (i_first < a.n_loc) select_predict_one(a, i_first, first, tn, tick, a.nact);
+    for (int i = i_first + gridDim.x * blockDim.x; i < a.n_loc; i += gridDim.x * blockDim.x) {
+        SelIn in;
+        load_sel_in(a, i, in);
+        select_predict_one(a, i, in, tn, tick, a.nact);
+    }
     if (!a.sel_done) return;
     // one shard: the last CTA to finish runs the decide step (block_decide_kernel's body)
     // -- every CTA's appends are complete and visible once it has taken its ticket
