@@ -423,9 +423,12 @@ __device__ void block_decide(long long* ctl, const unsigned long long* tnext, un
                 if (cur >= 0) cudaGraphKernelNodeSetEnabled(force_node(nodes, q, cur), false);
                 if (want >= 0) cudaGraphKernelNodeSetEnabled(force_node(nodes, q, want), true);
             }
-            if (want >= 0)
+            // the grid only when it changes (a kind switch resets it: the other node's grid
+            // may be stale)
+            if (want >= 0 && (cur != want || nodes->nb[q] != nb))
                 cudaGraphKernelNodeSetGridDim(force_node(nodes, q, want),
                                               dim3((unsigned)nb, (unsigned)nodes->chunks[q], 1));
+            nodes->nb[q] = want >= 0 ? nb : -1;
             nodes->cur[q] = want;
         }
         cudaGraphSetConditional(cond, done ? 0u : 1u);
@@ -541,18 +544,19 @@ __global__ void block_select_predict_kernel(StateArgs a) {
 // DADD each, instead of 192 64-bit shuffles + 192 DADD in every lane), and the next
 // round's loads are issued before this round's adds (C2 block steps 5.00 -> 4.68 ms per
 // dt_max, C3 76.0 -> 74.1, interleaved A/B against the shuffle form, profiles/r02_fold_ab.jsonl).
-__device__ __forceinline__ void fold_warp(const StateArgs& a, int q, int lane, double out[6],
-                                          double (*red)[6]) {
+// lane's values of the fold round starting at chunk c0 (0 past the last chunk)
+__device__ __forceinline__ void fold_load(const StateArgs& a, int q, int lane, int c0, double v[6]) {
     const double* p = a.partial + q;
     const int64_t row = a.n_loc_pad, stride = (int64_t)a.ncomp * a.n_loc_pad;
-    double s = 0.0;   // lane k < 6: component k
-    double v[6];
-    auto load = [&](int c0) {
-        const int c = c0 + lane;
+    const int c = c0 + lane;
 #pragma unroll
-        for (int k = 0; k < 6; ++k) v[k] = c < a.n_chunks ? p[c * stride + k * row] : 0.0;
-    };
-    load(0);
+    for (int k = 0; k < 6; ++k) v[k] = c < a.n_chunks ? p[c * stride + k * row] : 0.0;
+}
+// v: round 0 already loaded by the caller (fold_load(a, q, lane, 0, v))
+__device__ __forceinline__ void fold_warp(const StateArgs& a, int q, int lane, double v[6], double out[6],
+                                          double (*red)[6]) {
+    double s = 0.0;   // lane k < 6: component k
+    auto load = [&](int c0) { fold_load(a, q, lane, c0, v); };
     for (int c0 = 0; c0 < a.n_chunks; c0 += 32) {
         const int cnt = min(32, a.n_chunks - c0);
 #pragma unroll
@@ -580,15 +584,18 @@ __global__ void block_correct_kernel(StateArgs a) {
         __shared__ double red[kBlock / 32][32][6];   // one fold slab per warp
         const int lane = threadIdx.x & 31;
         for (int q = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5); q < n_act; q += nw) {
+            // the fold's first round does not depend on the slot's particle: its loads are
+            // issued with the active-list read, the state loads after it
+            double v[6];
+            fold_load(a, q, lane, 0, v);
             const int i = a.ilist[q];
             NB_CHECK(q < a.n_loc && i >= 0 && i < a.n_loc);
-            // lanes 0..2 load their component's state first (before the fold's loads)
             const int cc = lane < 3 ? lane : 0;
             const int64_t o = cc * a.n_loc_pad + i;
             const double a0 = a.a0[o], j0 = a.j0[o], xp = a.xp[o], vp = a.vp[o];
             const int k = a.lev[i];
             double f[6];
-            fold_warp(a, q, lane, f, red[threadIdx.x >> 5]);
+            fold_warp(a, q, lane, v, f, red[threadIdx.x >> 5]);
             // corrector: one lane per component, lane 0 sums the criterion's squares in
             // component order and sets the level (the arithmetic of correct_slot)
             const double dt = dt_of(a, k);

@@ -194,6 +194,7 @@ struct BlockGraphNodes {
     int32_t i_per_block, big_i_per_block, ts_i_per_block, ts1_i_per_block;
     int32_t ts_max, ts1_max;             // active counts <= ts1_max: scalar; <= ts_max: packed
     int32_t cur[8];                      // enabled force node per shard (kind, -1 none, -2 unknown)
+    int32_t nb[8];                       // ... and the grid x it was last given (-1 unknown)
 };
 cudaError_t launch_block_decide(long long* ctl, const unsigned long long* tnext, unsigned long long* tcur,
                                 int32_t* nact, int32_t* nact_cur, int nshards,

@@ -1031,7 +1031,7 @@ int block_run(nbody_ctx* c, int32_t nsteps) {
             hn.ts1_i_per_block = nb::force_tsplit_i_per_block(true);
             hn.ts_max = nb::force_tsplit_max();
             hn.ts1_max = nb::force_tsplit1_max();
-            for (int q = 0; q < 8; ++q) hn.cur[q] = -2;
+            for (int q = 0; q < 8; ++q) hn.cur[q] = -2, hn.nb[q] = -1;
             rc = block_step_body(c, cond, c->gnodes);
             if (!rc) rc = block_step_rest(c, nullptr, &hn);
             cudaGraph_t body = nullptr;
