@@ -1325,8 +1325,6 @@ int nbody_prof_read(nbody_ctx* c, double* force_ms, int64_t* force_launches, int
         // per block step select, force, correct per shard and decide; per call one last
         // iteration (select, decide, correct) that finds the run done
         const int64_t dk = decide_fused(c) ? 0 : 1;   // a separate decide launch
-        // per block step select, force, correct per shard and decide; per call one last
-        // iteration (select, decide, correct) that finds the run done
         graph_kernels = (3 * (int64_t)c->nshards + dk) * graph_steps +
                         (2 * (int64_t)c->nshards + dk) * c->block_graph_calls;
         if (reset) {
